@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark: Shifted Non-Local Search forward (search + top-L + softmax + wpsum aggregate) on
+B200, the BASELINE.json metric "search+aggregate queries/sec (ms/video) & %roofline".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+
+Workload (default c4 = BASELINE configs[3]): one 10x256x256x32 video per GPU, ws 11, wt 3,
+ps 3, k 16, L2, stride0 2, beta 1/288, fractional flows U[-2,2); Q = K = V as in the
+reference's run_benchmark (harness.cpp:242-270).  Inputs come from the reference's own
+generator UniformStream (seeds 100+b / 200+b / 300+b for video b = rank).
+Multi-GPU: videos are independent -> shard by batch, no data-path collective ("weak").
+
+A step = search (+ fused softmax epilogue) + wpsum on inputs resident in HBM; L2 (126 MB) is
+flushed with a 512 MB memset between steps, outside the timed events.  `e2e` repeats the
+step through the same public API from pinned HOST buffers with the H2D input copies and the
+D2H read-back of the results (sims, offsets, aggregated video) inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "search+aggregate queries/sec (ms/video) & %roofline at 1/2/4/8 B200 vs CPU ref"
+UNIT = "queries/s"
+
+WORKLOADS = {
+    # BASELINE configs[3]: batch=8 T=10 C=32 H=W=256 ws=11 wt=3 ps=3 k=16, one video per GPU
+    "c4": dict(T=10, H=256, W=256, C=32, ws=11, wt=3, ps=3, topl=16, metric="l2", stride0=2,
+               beta=1.0 / 288, vid_seed=100, ff_seed=200, bf_seed=300, flow_mag=2.0,
+               name="c4: 10x256x256x32 per video, ws11 wt3 ps3 k16 L2 s0=2, one video/GPU"),
+    # BASELINE configs[1]: T=5 C=64 H=W=128 ws=9 wt=2 ps=7 k=10 ip, stride0 4 (hole-free min)
+    "c2": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
+               beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0,
+               name="c2: 5x128x128x64, ws9 wt2 ps7 k10 ip s0=4"),
+}
+
+
+# ------------------------------------------------------------------------------------------
+# Work model: FMA-pipe lane instructions (FFMA/FADD/FMUL = 1) and compulsory bytes
+def work_model(wl):
+    T, H, W, C = wl["T"], wl["H"], wl["W"], wl["C"]
+    ws, wt, ps, s0, L = wl["ws"], wl["wt"], wl["ps"], wl["stride0"], wl["topl"]
+    m = 2 if wl["metric"] == "l2" else 1
+    nh, nw = (H - 1) // s0 + 1, (W - 1) // s0 + 1
+    per_frame_q = nh * nw
+    rows = T * per_frame_q
+    sim = interp = chain = 0
+    valid_slots = 0
+    for qt in range(T):
+        for dt in range(-wt, wt + 1):
+            if 0 <= qt + dt < T:
+                sim += per_frame_q * ws * ws * ps * ps * C * m
+                interp += per_frame_q * (ws + ps - 1) ** 2 * C * 4
+                chain += per_frame_q * 16 * max(abs(dt) - 1, 0)
+                valid_slots += per_frame_q * ws * ws
+    # wpsum: contributing units per pixel (footprint + cell completion, aggregate.cpp:156-188)
+    half = ps // 2
+    import numpy as np
+
+    def units_1d(n, ng):
+        cnt = np.zeros(n, np.int64)
+        for y in range(n):
+            c = sum(1 for py in range(-half, half + 1)
+                    if 0 <= y - py <= (ng - 1) * s0 and (y - py) % s0 == 0)
+            cnt[y] = c
+        own = np.minimum((np.arange(n) + (s0 - 1) // 2) // s0, ng - 1) * s0
+        far = np.abs(np.arange(n) - own) > half
+        return cnt, far
+
+    cy, fy = units_1d(H, nh)
+    cx, fx = units_1d(W, nw)
+    units = np.outer(cy, cx) + (fy[:, None] | fx[None, :])
+    contrib = int(units.sum()) * T
+    wpsum = contrib * L * C * 5 + T * H * W * C
+    vid = T * H * W * C * 4
+    flows = 2 * T * H * W * 2 * 4
+    b_search = vid + flows + rows * L * (4 + 12 + 4)  # Q=K aliased; sims+offsets+weights
+    b_wpsum = vid + rows * L * 16 + vid + T * H * W * 4
+    return dict(rows=rows, search_instr=sim + interp + chain, search_sim=sim, search_interp=interp,
+                wpsum_instr=wpsum, bytes_search=b_search, bytes_wpsum=b_wpsum,
+                valid_slots_per_query=valid_slots / rows)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def make_inputs(S, wl, b):
+    import numpy as np
+
+    T, H, W, C = wl["T"], wl["H"], wl["W"], wl["C"]
+    vid = S.uniform_fill(wl["vid_seed"] + b, -1.0, 1.0, T * H * W * C).reshape(T, H, W, C)
+    ff = S.uniform_fill(wl["ff_seed"] + b, -wl["flow_mag"], wl["flow_mag"], T * H * W * 2)
+    bf = S.uniform_fill(wl["bf_seed"] + b, -wl["flow_mag"], wl["flow_mag"], T * H * W * 2)
+    return vid, ff.reshape(T, H, W, 2), bf.reshape(T, H, W, 2)
+
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_16849_b200 import snls as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    model = work_model(wl)
+    rows = model["rows"]
+    cfg = S.SearchConfig(ws=wl["ws"], wt=wl["wt"], ps=wl["ps"], stride0=wl["stride0"],
+                         stride1=1.0, topl=wl["topl"], metric=wl["metric"], softmax_scale=wl["beta"])
+    vid_h, ff_h, bf_h = make_inputs(S, wl, rank)
+    vid = torch.from_numpy(vid_h).to(dev)
+    ff = torch.from_numpy(ff_h).to(dev)
+    bf = torch.from_numpy(bf_h).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = S.context(local)
+    L = wl["topl"]
+    sims = torch.empty((rows, L), device=dev)
+    offs = torch.empty((rows, L, 3), device=dev)
+    wts = torch.empty((rows, L), device=dev)
+    out = torch.empty_like(vid)
+    counts = torch.empty(vid.shape[:3], device=dev, dtype=torch.int32)
+    flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
+
+    def step():
+        S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
+                              out=(sims, offs, None, wts))
+        ev_mid.record(stream)
+        S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts))
+
+    # correctness gate before timing: device error latch must be clean
+    ev_mid = torch.cuda.Event(enable_timing=True)
+    step()
+    ctx.sync_check()
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        ev_mid = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e2.record(stream)
+        evs.append((e0, ev_mid, e2))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    ctx.sync_check()
+    step_ms = [a.elapsed_time(c) for a, _, c in evs]
+    search_ms = [a.elapsed_time(b) for a, b, _ in evs]
+    wpsum_ms = [b.elapsed_time(c) for _, b, c in evs]
+    tot = sum(step_ms)
+    tot_search = sum(search_ms)
+    if world > 1:
+        t = torch.tensor([tot, tot_search], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot, tot_search = float(t[0]), float(t[1])
+    ms_per_step = tot / args.steps
+
+    # ---- e2e: pinned host buffers, copies inside the timed region ----
+    vid_p = torch.from_numpy(vid_h).pin_memory()
+    ff_p, bf_p = torch.from_numpy(ff_h).pin_memory(), torch.from_numpy(bf_h).pin_memory()
+    sims_p = torch.empty((rows, L)).pin_memory()
+    offs_p = torch.empty((rows, L, 3)).pin_memory()
+    out_p = torch.empty(vid_h.shape).pin_memory()
+    vd, ffd, bfd = torch.empty_like(vid), torch.empty_like(ff), torch.empty_like(bf)
+
+    def e2e_step():
+        vd.copy_(vid_p, non_blocking=True)
+        ffd.copy_(ff_p, non_blocking=True)
+        bfd.copy_(bf_p, non_blocking=True)
+        S.shifted_nls_forward(vd, vd, ffd, bfd, cfg, ctx=ctx, check=False,
+                              out=(sims, offs, None, wts))
+        S.wpsum(vd, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts))
+        sims_p.copy_(sims, non_blocking=True)
+        offs_p.copy_(offs, non_blocking=True)
+        out_p.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_e2e = max(3, min(args.steps, 10))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n_e2e):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / n_e2e
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    ctx.sync_check()
+    h2d = vid_h.nbytes + ff_h.nbytes + bf_h.nbytes
+    d2h = sims_p.numel() * 4 + offs_p.numel() * 4 + out_p.numel() * 4
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    P, peak_src = peaks()
+    sm_max = float(P.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak_tflops = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    t_search = tot_search / args.steps / 1e3
+    achieved = 2.0 * model["search_instr"] / t_search / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.workload, {}).get("search_bytes_per_launch")
+        except Exception:
+            traffic = None
+    result = {
+        "metric": METRIC,
+        "value": rows * world / (ms_per_step / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "ms_per_video": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: reference UniformStream video U[-1,1) (Q=K=V) and flows U[-2,2)",
+        "config": {"workload": wl["name"], "videos_per_gpu": 1, "queries_per_video": rows,
+                   "parallelism": f"batch-sharded x{world} (no collective)",
+                   "l2": "flushed (512 MB memset) between timed steps"},
+        "breakdown_ms": {"search_topl_softmax": tot_search / args.steps,
+                         "wpsum": statistics.mean(wpsum_ms)},
+        "roofline": {"bound": "fp32", "kernel": "search_tiled_kernel",
+                     "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak_tflops, "traffic": traffic,
+                     "algorithmic": f"{model['search_instr']:.4g} FMA-pipe instr/video x2 flop",
+                     "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x sm_max_mhz from {peak_src}",
+                     "hbm_frac": model["bytes_search"] / t_search / 1e9 / float(P.get("hbm_gbs", 6650))},
+        "e2e": {"value": rows * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "wall_s_timed_loop": wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
+    print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------
+def reference_sample(wl, crop):
+    """The reference's own CPU path (oracle/_ref: unmodified sources, OpenMP, fp64) on a crop
+    of the workload with identical per-query work (same ws/wt/ps/k/metric/stride0/C/T)."""
+    import numpy as np
+
+    from oracle.oracle import Cfg, Checker
+
+    R = Checker("reference")
+    T, C = wl["T"], wl["C"]
+    H = W = crop
+    v = R.uniform(wl["vid_seed"], -1, 1, T * H * W * C).astype(np.float32).astype(np.float64)
+    v = v.reshape(T, H, W, C)
+    ff = R.uniform(wl["ff_seed"], -2, 2, T * H * W * 2).astype(np.float32).astype(np.float64)
+    bf = R.uniform(wl["bf_seed"], -2, 2, T * H * W * 2).astype(np.float32).astype(np.float64)
+    ff, bf = ff.reshape(T, H, W, 2), bf.reshape(T, H, W, 2)
+    cfg = Cfg(ws=wl["ws"], wt=wl["wt"], ps=wl["ps"], stride0=wl["stride0"], stride1=1.0,
+              topl=wl["topl"], metric=wl["metric"], softmax_scale=wl["beta"])
+    rows = T * ((H - 1) // cfg.stride0 + 1) * ((W - 1) // cfg.stride0 + 1)
+
+    def run():
+        t0 = time.perf_counter()
+        r = R.search_fwd(v, v, ff, bf, cfg)
+        w = R.softmax_rows(r["sims"], cfg.softmax_scale)
+        R.wpsum(v, w, r["offsets"], cfg)
+        return time.perf_counter() - t0
+
+    return R, rows, run
+
+
+def cpu_baseline(wl, budget_s=20.0):
+    crop = 96
+    R, rows, run = reference_sample(wl, crop)
+    t = run()  # warm-up + size probe
+    times = []
+    deadline = time.perf_counter() + budget_s
+    while len(times) < 3 or (time.perf_counter() < deadline and len(times) < 9):
+        times.append(run())
+        if time.perf_counter() > deadline and len(times) >= 1:
+            break
+    med = statistics.median(times)
+    return {"value": rows / med, "unit": UNIT, "cores": R.lib.ref_max_threads(),
+            "kind": "reference",
+            "sample": (f"reference snls::shifted_nls_forward + softmax_rows + wpsum (oracle/_ref, "
+                       f"fp64, OpenMP all host threads) on a {wl['T']}x{crop}x{crop}x{wl['C']} crop "
+                       f"of the workload ({rows} queries, identical per-query work), median of "
+                       f"{len(times)} runs after 1 warm-up ({t:.2f}s)")}
+
+
+def run_reference(args, wl):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    crop = args.ref_crop
+    R, rows, run = reference_sample(wl, crop)
+    for _ in range(args.warmup):
+        run()
+    times = [run() for _ in range(args.steps)]
+    tot = sum(times)
+    value = rows * args.steps / tot
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference UniformStream video U[-1,1) (Q=K=V) and flows U[-2,2)",
+        "config": {"workload": wl["name"], "sample": f"{wl['T']}x{crop}x{crop}x{wl['C']} crop",
+                   "queries_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": R.lib.ref_max_threads(),
+                         "kind": "reference",
+                         "sample": f"{wl['T']}x{crop}x{crop}x{wl['C']} crop, {rows} queries/step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-crop", type=int, default=96)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/* snls_cuda.h -- C-ABI of the B200 (sm_100a) Shifted Non-Local Search library.
+ *
+ * This is the thin shim the reference's C++ API calls through: the drop-in adapter
+ * (paper_2309_16849_b200/host/snls_gpu_search.cpp, snls_gpu_aggregate.cpp) implements the
+ * reference's `snls::` entry points (search.hpp:126-158, aggregate.hpp:22-85) by converting
+ * the fp64 host containers to fp32 device buffers and calling the functions below.  The
+ * Python tests and bench.py call the same functions through ctypes.
+ *
+ * Conventions
+ *  - extern "C", no exceptions, no STL, no torch types.  Every function returns an
+ *    snls_status; the message of the last failure on the calling thread is
+ *    snls_last_error().  Validation failures carry the reference's exact messages
+ *    (ConfigError -> SNLS_ECONFIG, DomainError -> SNLS_EDOMAIN).
+ *  - Tensor arguments are DEVICE pointers to fp32 (counts: int32), row-major with the
+ *    reference's layouts: videos T x H x W x F (F fastest, tensor.hpp:17-31), flows
+ *    T x H x W x 2 holding (dy, dx) (flow.hpp:12-28), query rows (t, y, x) with x fastest
+ *    on the grid {0, stride0, ...} (search.hpp:47-55).
+ *  - Work is enqueued on the context's stream and returns immediately.  Domain errors that
+ *    only the device can see (non-finite flows, offsets leaving the clip, non-finite
+ *    softmax inputs) are latched in the context and reported by snls_ctx_sync_check().
+ *
+ * The search tape.  The reference's SearchTape (search.hpp:89-110) stores absolute key
+ * centres and absolute chain positions in fp64.  The device tape stores what fp32 can hold
+ * exactly enough: `offsets` (dt, ky-qy, kx-qx) per selected entry (centres = query + offset)
+ * and `chains` rows x L x max(wt-1,0) x 6 links (pos_y-qy, pos_x-qx, J00, J01, J10, J11),
+ * positions relative to the query pixel.
+ */
+#ifndef SNLS_CUDA_H
+#define SNLS_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNLS_CUDA_ABI_VERSION 1
+
+typedef enum {
+    SNLS_OK = 0,
+    SNLS_ECONFIG = 1, /* snls::ConfigError (errors.hpp:9-12) */
+    SNLS_EDOMAIN = 2, /* snls::DomainError (errors.hpp:14-17) */
+    SNLS_ECUDA = 3,   /* CUDA runtime failure, no device, or the kernels are not loadable */
+    SNLS_EARG = 4     /* null or inconsistent argument at the C boundary */
+} snls_status;
+
+typedef enum { SNLS_METRIC_IP = 0, SNLS_METRIC_L2 = 1 } snls_metric; /* search.hpp:12 */
+
+typedef enum { SNLS_MODE_FUSED = 0, SNLS_MODE_FULLGRID = 1 } snls_mode; /* search.hpp:37 */
+
+/* snls::SearchConfig (search.hpp:17-35), field for field. */
+typedef struct {
+    int ws;               /* spatial window size, odd */
+    int wt;               /* temporal radius */
+    int ps;               /* patch size, odd */
+    int stride0;          /* query stride */
+    double stride1;       /* key stride (fractional allowed) */
+    int topl;             /* neighbours kept per query */
+    int metric;           /* snls_metric */
+    double softmax_scale; /* beta for the fused softmax epilogue / softmax_rows */
+} snls_config;
+
+typedef struct {
+    int t, h, w, f;
+} snls_dims;
+
+typedef struct snls_ctx snls_ctx;
+
+/* ---- host-only helpers (no device needed) ------------------------------------------ */
+int snls_abi_version(void);
+const char* snls_last_error(void);
+/* SearchConfig::validate (search.cpp:21-32) */
+int snls_validate_config(const snls_config* cfg);
+/* QueryGrid::over (search.cpp:43-50) */
+int snls_query_grid(snls_dims dims, int stride0, int64_t* rows, int* nh, int* nw);
+/* UniformStream(seed).next_in(lo, hi) (rng.hpp:12-24) rounded to fp32, into HOST memory;
+ * the synthetic-input generator of run_benchmark (harness.cpp:242-253). */
+int snls_uniform_fill_f32(uint64_t seed, double lo, double hi, int64_t n, float* host_out);
+
+/* ---- context: one per (device, stream) --------------------------------------------- */
+int snls_ctx_create(int device, void* cuda_stream, snls_ctx** out);
+int snls_ctx_destroy(snls_ctx* ctx);
+int snls_ctx_set_stream(snls_ctx* ctx, void* cuda_stream);
+/* Synchronise the stream; report (and clear) latched device-side domain errors. */
+int snls_ctx_sync_check(snls_ctx* ctx);
+/* Number of kernels this context has launched (evidence for bench.py's gpu_launches). */
+int snls_ctx_launch_count(snls_ctx* ctx, int64_t* out);
+/* Kernel path the last search_fwd took: 0 generic per-slot, 1 tiled stride1 == 1. */
+int snls_ctx_last_search_path(snls_ctx* ctx, int* out);
+/* Force the generic per-slot search path (1) or allow the tiled one (0, default). */
+int snls_ctx_force_generic(snls_ctx* ctx, int on);
+
+/* ---- search (search.hpp) ------------------------------------------------------------ */
+/* Replaces snls::shifted_nls_forward (search.hpp:126-128; search.cpp:414-421).
+ * fflow/bflow may be NULL for zero flows (snls::nls_forward, search.hpp:131-132).
+ * Outputs: sims rows x L (best first), offsets rows x L x 3, optional chains (see above,
+ * NULL to skip), optional weights rows x L = softmax_rows(sims, cfg.softmax_scale) fused in
+ * the epilogue (NULL to skip).  mode SNLS_MODE_FULLGRID materialises the rows x
+ * window_slots score grid in a context workspace before selection, as the reference's
+ * kFullGrid does (search.cpp:329-410); results are identical to SNLS_MODE_FUSED. */
+int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                    const float* k, const float* fflow, const float* bflow, int mode,
+                    float* sims, float* offsets, float* chains, float* weights);
+
+/* The pre-selection score grid rows x window_slots (-inf on off-clip frames) and its
+ * offsets rows x window_slots x 3, as full_grid_forward builds it (search.cpp:351-376). */
+int snls_search_grid(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                     const float* k, const float* fflow, const float* bflow, float* grid,
+                     float* grid_offsets);
+
+/* Replaces snls::top_l (search.hpp:137-138; search.cpp:430-468). */
+int snls_topl(snls_ctx* ctx, int64_t rows, int cols, const float* full,
+              const float* full_offsets, int topl, float* sel, float* sel_offsets);
+
+/* Replaces snls::replay_similarities (search.hpp:157-158; search.cpp:470-493). */
+int snls_replay(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                const float* k, const float* offsets, float* sims);
+
+/* Replaces snls::shifted_nls_backward (search.hpp:151-153; search.cpp:671-711).
+ * Gradients are accumulated with atomics (the reference's non-deterministic mode); the
+ * four outputs are overwritten (zeroed first).  dfflow/dbflow T x H x W x 2. */
+int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
+                    const float* grad_sims, const float* offsets, const float* chains,
+                    const float* q, const float* k, float* dq, float* dk, float* dfflow,
+                    float* dbflow);
+
+/* ---- aggregate (aggregate.hpp) ------------------------------------------------------ */
+/* Replaces snls::softmax_rows (aggregate.hpp:22; aggregate.cpp:16-37). */
+int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims,
+                      float* weights);
+
+/* Replaces snls::wpsum (aggregate.hpp:53-54; deterministic gather, aggregate.cpp:124-203).
+ * out T x H x W x F, counts T x H x W (the AggTape, aggregate.hpp:27-36). */
+int snls_wpsum_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
+                   const float* weights, const float* offsets, float* out, int32_t* counts);
+
+/* Replaces snls::gather_stack (aggregate.hpp:71-73; aggregate.cpp:285-347).
+ * out L x T x H x W x F. */
+int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
+                      const float* weights, const float* offsets, float* out);
+
+/* Replaces snls::wpsum_backward (aggregate.hpp:83-85; aggregate.cpp:412-460).
+ * dv T x H x W x F, dweights rows x L; both overwritten. */
+int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
+                   const float* grad_out, const int32_t* counts, const float* v,
+                   const float* weights, const float* offsets, float* dv, float* dweights);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNLS_CUDA_H */

@@ -1,0 +1,438 @@
+// The C-ABI (include/snls_cuda.h): validation with the reference's messages, dispatch to
+// the sm_100a kernels, and the per-(device, stream) context.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "snls_cuda.h"
+
+using namespace snls_gpu;
+
+struct snls_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int* err = nullptr;  // device-side latch
+    void* work = nullptr;
+    size_t work_bytes = 0;
+    int64_t launches = 0;
+    int num_sms = 148;
+    int force_generic = 0;
+    int last_path = -1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(SNLS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int after_launch(snls_ctx* ctx, int launched, const char* where) {
+    if (launched > 0) ctx->launches += launched;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, where);
+    return SNLS_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// search.cpp:21-32, messages verbatim
+int validate(const snls_config* c) {
+    if (!c) return fail(SNLS_EARG, "snls: null config");
+    if (c->ws < 1 || c->ws % 2 == 0)
+        return fail(SNLS_ECONFIG, "SearchConfig: ws must be odd and positive");
+    if (c->ps < 1 || c->ps % 2 == 0)
+        return fail(SNLS_ECONFIG, "SearchConfig: ps must be odd and positive");
+    if (c->wt < 0) return fail(SNLS_ECONFIG, "SearchConfig: wt must be >= 0");
+    if (c->stride0 < 1) return fail(SNLS_ECONFIG, "SearchConfig: stride0 must be >= 1");
+    if (!(c->stride1 > 0.0) || !std::isfinite(c->stride1))
+        return fail(SNLS_ECONFIG, "SearchConfig: stride1 must be positive and finite");
+    const long long slots = (2LL * c->wt + 1) * c->ws * c->ws;
+    if (c->topl < 1 || c->topl > slots)
+        return fail(SNLS_ECONFIG, "SearchConfig: topl must lie in [1, window slots]");
+    if (!std::isfinite(c->softmax_scale))
+        return fail(SNLS_ECONFIG, "SearchConfig: softmax_scale must be finite");
+    if (c->metric != SNLS_METRIC_IP && c->metric != SNLS_METRIC_L2)
+        return fail(SNLS_ECONFIG, "SearchConfig: unknown metric");
+    return SNLS_OK;
+}
+
+int check_dims(snls_dims d) {
+    if (d.t < 1 || d.h < 1 || d.w < 1 || d.f < 1)
+        return fail(SNLS_EDOMAIN, "VideoTensor: all extents must be at least 1");
+    return SNLS_OK;
+}
+
+int check_ctx(snls_ctx* ctx) {
+    if (!ctx) return fail(SNLS_EARG, "snls: null context");
+    return SNLS_OK;
+}
+
+// fused_forward's underfull rule (search.cpp:317-325), decided from shapes alone: the
+// fewest valid frames any query frame sees, times ws^2.
+bool underfull(const snls_config* c, int t) {
+    long long worst = -1;
+    for (int qt = 0; qt < t; ++qt) {
+        const int lo = qt - c->wt < 0 ? 0 : qt - c->wt;
+        const int hi = qt + c->wt > t - 1 ? t - 1 : qt + c->wt;
+        const long long valid = (long long)(hi - lo + 1) * c->ws * c->ws;
+        if (worst < 0 || valid < worst) worst = valid;
+    }
+    return worst < c->topl;
+}
+
+int ensure_work(snls_ctx* ctx, size_t bytes) {
+    if (ctx->work_bytes >= bytes) return SNLS_OK;
+    if (ctx->work) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->work);
+        ctx->work = nullptr;
+        ctx->work_bytes = 0;
+    }
+    const cudaError_t e = cudaMalloc(&ctx->work, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "snls workspace");
+    ctx->work_bytes = bytes;
+    return SNLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int snls_abi_version(void) { return SNLS_CUDA_ABI_VERSION; }
+
+const char* snls_last_error(void) { return g_err.c_str(); }
+
+int snls_validate_config(const snls_config* cfg) { return validate(cfg); }
+
+int snls_query_grid(snls_dims dims, int stride0, int64_t* rows, int* nh, int* nw) {
+    if (stride0 < 1) return fail(SNLS_ECONFIG, "SearchConfig: stride0 must be >= 1");
+    if (int rc = check_dims(dims)) return rc;
+    const Dims d = make_dims(dims, stride0);
+    if (rows) *rows = d.rows;
+    if (nh) *nh = d.nh;
+    if (nw) *nw = d.nw;
+    return SNLS_OK;
+}
+
+// std::mt19937_64 + UniformStream::next_in (rng.hpp:12-24), rounded to fp32.
+int snls_uniform_fill_f32(uint64_t seed, double lo, double hi, int64_t n, float* out) {
+    if (!out && n > 0) return fail(SNLS_EARG, "snls_uniform_fill_f32: null output");
+    uint64_t mt[312];
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+    int idx = 312;
+    for (int64_t i = 0; i < n; ++i) {
+        if (idx >= 312) {
+            for (int j = 0; j < 312; ++j) {
+                const uint64_t x = (mt[j] & 0xFFFFFFFF80000000ULL) | (mt[(j + 1) % 312] & 0x7FFFFFFFULL);
+                uint64_t xa = x >> 1;
+                if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+                mt[j] = mt[(j + 156) % 312] ^ xa;
+            }
+            idx = 0;
+        }
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ULL;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+        y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+        y ^= y >> 43;
+        out[i] = float(lo + (hi - lo) * (double(y >> 11) * 0x1.0p-53));
+    }
+    return SNLS_OK;
+}
+
+int snls_ctx_create(int device, void* stream, snls_ctx** out) {
+    if (!out) return fail(SNLS_EARG, "snls_ctx_create: null output");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return fail(SNLS_ECUDA, "snls_ctx_create: no CUDA device visible");
+    if (device < 0 || device >= n) return fail(SNLS_EARG, "snls_ctx_create: device index out of range");
+    DeviceGuard g(device);
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "snls_ctx_create");
+    if (prop.major != 10)
+        return fail(SNLS_ECUDA, std::string("snls_ctx_create: kernels are built for sm_100a, device is ") +
+                                    prop.name);
+    snls_ctx* ctx = new snls_ctx();
+    ctx->device = device;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->num_sms = prop.multiProcessorCount;
+    if ((e = cudaMalloc(&ctx->err, sizeof(int))) != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "snls_ctx_create");
+    }
+    cudaMemset(ctx->err, 0, sizeof(int));
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+        cudaFree(ctx->err);
+        delete ctx;
+        return cuda_fail(e, "snls_ctx_create");
+    }
+    *out = ctx;
+    return SNLS_OK;
+}
+
+int snls_ctx_destroy(snls_ctx* ctx) {
+    if (!ctx) return SNLS_OK;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->err) cudaFree(ctx->err);
+    if (ctx->work) cudaFree(ctx->work);
+    delete ctx;
+    return SNLS_OK;
+}
+
+int snls_ctx_set_stream(snls_ctx* ctx, void* stream) {
+    if (int rc = check_ctx(ctx)) return rc;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return SNLS_OK;
+}
+
+int snls_ctx_launch_count(snls_ctx* ctx, int64_t* out) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (out) *out = ctx->launches;
+    return SNLS_OK;
+}
+
+int snls_ctx_last_search_path(snls_ctx* ctx, int* out) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (out) *out = ctx->last_path;
+    return SNLS_OK;
+}
+
+int snls_ctx_force_generic(snls_ctx* ctx, int on) {
+    if (int rc = check_ctx(ctx)) return rc;
+    ctx->force_generic = on;
+    return SNLS_OK;
+}
+
+int snls_ctx_sync_check(snls_ctx* ctx) {
+    if (int rc = check_ctx(ctx)) return rc;
+    DeviceGuard g(ctx->device);
+    int host = 0;
+    cudaError_t e = cudaMemcpyAsync(&host, ctx->err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_ctx_sync_check");
+    if (host == 0) return SNLS_OK;
+    cudaMemsetAsync(ctx->err, 0, sizeof(int), ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    if (host & kErrFflow) return fail(SNLS_EDOMAIN, "search fflow: flow holds a non-finite value");
+    if (host & kErrBflow) return fail(SNLS_EDOMAIN, "search bflow: flow holds a non-finite value");
+    if (host & kErrSoftmax) return fail(SNLS_EDOMAIN, "softmax_rows: non-finite input");
+    if (host & kErrWpsum)
+        return fail(SNLS_EDOMAIN, "wpsum: offsets leave the clip or a pixel has no writers");
+    if (host & kErrStack) return fail(SNLS_EDOMAIN, "gather_stack: offsets leave the clip");
+    if (host & kErrTopl) return fail(SNLS_EDOMAIN, "top_l: some row has fewer than L valid entries");
+    return fail(SNLS_EDOMAIN, "snls: device reported an unknown domain error");
+}
+
+static int search_common_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
+                                const float* q, const float* k, const float* ff, const float* bf) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if (!q || !k) return fail(SNLS_EARG, "search: null query/key tensor");
+    if ((ff == nullptr) != (bf == nullptr))
+        return fail(SNLS_EARG, "search: pass both flows or neither (nls_forward)");
+    return SNLS_OK;
+}
+
+int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                    const float* k, const float* ff, const float* bf, int mode, float* sims,
+                    float* offsets, float* chains, float* weights) {
+    if (int rc = search_common_checks(ctx, cfg, dims, q, k, ff, bf)) return rc;
+    if (!sims || !offsets) return fail(SNLS_EARG, "search: null output");
+    if (underfull(cfg, dims.t))
+        return fail(SNLS_ECONFIG, "search: topl exceeds the valid window entries of some query");
+    DeviceGuard g(ctx->device);
+    const Dims d = make_dims(dims, cfg->stride0);
+    const int64_t nflow = int64_t(dims.t) * dims.h * dims.w * 2;
+    int launched = launch_flows_check(ff, bf, nflow, ctx->err, ctx->stream);
+    const float beta = float(cfg->softmax_scale);
+
+    if (mode == SNLS_MODE_FULLGRID) {
+        const int n = (2 * cfg->wt + 1) * cfg->ws * cfg->ws;
+        const size_t need = size_t(d.rows) * n * 4 * sizeof(float);
+        if (int rc = ensure_work(ctx, need)) return rc;
+        float* grid = static_cast<float*>(ctx->work);
+        float* goff = grid + size_t(d.rows) * n;
+        GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
+                         cfg->stride1, beta, sims, offsets, nullptr, nullptr, grid, goff, 0, ctx->err};
+        if (launch_search_generic(gs, ctx->stream) < 0)
+            return fail(SNLS_ECONFIG, "search: window too large for the device search");
+        ++launched;
+        if (launch_topl(d.rows, n, grid, goff, cfg->topl, sims, offsets, ctx->err, ctx->stream) < 0)
+            return fail(SNLS_ECONFIG, "search: window too large for the device top_l");
+        ++launched;
+        if (chains && cfg->wt > 1)
+            launched += launch_emit_tape(ff, bf, d, cfg->wt, cfg->topl, offsets, chains, ctx->stream);
+        if (weights) launched += launch_softmax(d.rows, cfg->topl, beta, sims, weights, ctx->err, ctx->stream);
+        ctx->last_path = 0;
+        return after_launch(ctx, launched, "snls_search_fwd(fullgrid)");
+    }
+
+    int tiled = 0;
+    if (!ctx->force_generic && cfg->stride1 == 1.0) {
+        TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
+                       sims, offsets, chains, weights, ctx->err, ctx->num_sms};
+        tiled = launch_search_tiled(ts, ctx->stream);
+        if (tiled < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
+    }
+    if (tiled > 0) {
+        launched += tiled;
+        ctx->last_path = 1;
+    } else {
+        GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
+                         cfg->stride1, beta, sims, offsets, chains, weights, nullptr, nullptr, 1, ctx->err};
+        if (launch_search_generic(gs, ctx->stream) < 0)
+            return fail(SNLS_ECONFIG, "search: window too large for the device search");
+        ++launched;
+        ctx->last_path = 0;
+    }
+    return after_launch(ctx, launched, "snls_search_fwd");
+}
+
+int snls_search_grid(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                     const float* k, const float* ff, const float* bf, float* grid,
+                     float* grid_offsets) {
+    if (int rc = search_common_checks(ctx, cfg, dims, q, k, ff, bf)) return rc;
+    if (!grid) return fail(SNLS_EARG, "search_grid: null output");
+    DeviceGuard g(ctx->device);
+    const Dims d = make_dims(dims, cfg->stride0);
+    int launched = launch_flows_check(ff, bf, int64_t(dims.t) * dims.h * dims.w * 2, ctx->err, ctx->stream);
+    GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
+                     cfg->stride1, 1.f, nullptr, nullptr, nullptr, nullptr, grid, grid_offsets, 0, ctx->err};
+    if (launch_search_generic(gs, ctx->stream) < 0)
+        return fail(SNLS_ECONFIG, "search: window too large for the device search");
+    return after_launch(ctx, launched + 1, "snls_search_grid");
+}
+
+int snls_topl(snls_ctx* ctx, int64_t rows, int cols, const float* full, const float* full_offsets,
+              int topl, float* sel, float* sel_offsets) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (rows < 0 || cols < 1) return fail(SNLS_EDOMAIN, "top_l: similarity and offset shapes disagree");
+    if (topl < 1 || topl > cols) return fail(SNLS_ECONFIG, "top_l: L out of range");
+    if (rows == 0) return SNLS_OK;
+    if (!full || !full_offsets || !sel || !sel_offsets) return fail(SNLS_EARG, "top_l: null tensor");
+    DeviceGuard g(ctx->device);
+    if (launch_topl(rows, cols, full, full_offsets, topl, sel, sel_offsets, ctx->err, ctx->stream) < 0)
+        return fail(SNLS_ECONFIG, "top_l: row too long for the device selection");
+    return after_launch(ctx, 1, "snls_topl");
+}
+
+int snls_replay(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
+                const float* k, const float* offsets, float* sims) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if (!q || !k || !offsets || !sims) return fail(SNLS_EARG, "replay_similarities: null tensor");
+    DeviceGuard g(ctx->device);
+    const Dims d = make_dims(dims, cfg->stride0);
+    return after_launch(ctx, launch_replay(q, k, d, cfg->ps, cfg->metric, cfg->topl, offsets, sims, ctx->stream),
+                        "snls_replay");
+}
+
+int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad,
+                    const float* offsets, const float* chains, const float* q, const float* k,
+                    float* dq, float* dk, float* dff, float* dbf) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if (!grad || !offsets || !q || !k || !dq || !dk || !dff || !dbf)
+        return fail(SNLS_EARG, "shifted_nls_backward: null tensor");
+    if (cfg->wt > 1 && !chains)
+        return fail(SNLS_EARG, "shifted_nls_backward: the tape needs chains when wt > 1");
+    DeviceGuard g(ctx->device);
+    const Dims d = make_dims(dims, cfg->stride0);
+    const size_t nv = size_t(dims.t) * dims.h * dims.w;
+    cudaMemsetAsync(dq, 0, nv * dims.f * sizeof(float), ctx->stream);
+    cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
+    cudaMemsetAsync(dff, 0, nv * 2 * sizeof(float), ctx->stream);
+    cudaMemsetAsync(dbf, 0, nv * 2 * sizeof(float), ctx->stream);
+    const size_t scratch = size_t(d.rows) * cfg->topl * 2 * sizeof(double);
+    if (int rc = ensure_work(ctx, scratch)) return rc;
+    cudaMemsetAsync(ctx->work, 0, scratch, ctx->stream);
+    const int n = launch_search_bwd_impl(grad, offsets, chains, q, k, d, cfg->wt, cfg->ps, cfg->topl,
+                                         cfg->metric, dq, dk, dff, dbf, static_cast<double*>(ctx->work),
+                                         ctx->stream);
+    return after_launch(ctx, n, "snls_search_bwd");
+}
+
+int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims, float* weights) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (rows < 0 || l < 1) return fail(SNLS_EDOMAIN, "softmax_rows: bad shape");
+    if (rows == 0) return SNLS_OK;
+    if (!sims || !weights) return fail(SNLS_EARG, "softmax_rows: null tensor");
+    DeviceGuard g(ctx->device);
+    return after_launch(ctx, launch_softmax(rows, l, float(beta), sims, weights, ctx->err, ctx->stream),
+                        "snls_softmax_rows");
+}
+
+// check_agg_inputs (aggregate.cpp:47-66)
+static int agg_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
+                      const float* w, const float* o) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (!((cfg->ps - 1) / 2 < cfg->stride0))
+        return fail(SNLS_ECONFIG, "aggregate: (ps-1)/2 < stride0 is required for hole-free output");
+    if (int rc = check_dims(dims)) return rc;
+    if (!v || !w || !o) return fail(SNLS_EARG, "aggregate: null tensor");
+    return SNLS_OK;
+}
+
+int snls_wpsum_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
+                   const float* weights, const float* offsets, float* out, int32_t* counts) {
+    if (int rc = agg_checks(ctx, cfg, dims, v, weights, offsets)) return rc;
+    if (!out) return fail(SNLS_EARG, "wpsum: null output");
+    DeviceGuard g(ctx->device);
+    AggArgs a{v, weights, offsets, make_dims(dims, cfg->stride0), cfg->ps, cfg->topl, ctx->err};
+    return after_launch(ctx, launch_wpsum(a, out, counts, ctx->stream), "snls_wpsum_fwd");
+}
+
+int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
+                      const float* weights, const float* offsets, float* out) {
+    if (int rc = agg_checks(ctx, cfg, dims, v, weights, offsets)) return rc;
+    if (!out) return fail(SNLS_EARG, "gather_stack: null output");
+    DeviceGuard g(ctx->device);
+    AggArgs a{v, weights, offsets, make_dims(dims, cfg->stride0), cfg->ps, cfg->topl, ctx->err};
+    return after_launch(ctx, launch_gather_stack(a, out, ctx->stream), "snls_gather_stack");
+}
+
+int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad_out,
+                   const int32_t* counts, const float* v, const float* weights, const float* offsets,
+                   float* dv, float* dw) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if (!grad_out || !counts || !v || !weights || !offsets || !dv || !dw)
+        return fail(SNLS_EARG, "wpsum_backward: null tensor");
+    DeviceGuard g(ctx->device);
+    const Dims d = make_dims(dims, cfg->stride0);
+    cudaMemsetAsync(dv, 0, size_t(dims.t) * dims.h * dims.w * dims.f * sizeof(float), ctx->stream);
+    cudaMemsetAsync(dw, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
+    AggArgs a{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err};
+    return after_launch(ctx, launch_wpsum_bwd(a, grad_out, counts, dv, dw, ctx->stream), "snls_wpsum_bwd");
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// Shared device helpers for the sm_100a Shifted Non-Local Search kernels.
+//
+// Numerics: tensors are fp32 in HBM and the patch arithmetic is fp32 (FFMA pipe).  Sample
+// positions are never formed as one fp32 number (qy + shift loses ~3e-5 relative at 512
+// px): a position is an integer base plus an fp32 fraction, and flow shifts are
+// accumulated in fp64 registers (once per query x frame, off the hot loop).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "snls_cuda.h"
+
+namespace snls_gpu {
+
+// Device-side domain-error latch bits (reported by snls_ctx_sync_check).
+enum : int {
+    kErrFflow = 1,      // "search fflow: flow holds a non-finite value"   flow.cpp:20-23
+    kErrBflow = 2,      // "search bflow: flow holds a non-finite value"
+    kErrSoftmax = 4,    // "softmax_rows: non-finite input"                 aggregate.cpp:25
+    kErrWpsum = 8,      // "wpsum: offsets leave the clip or a pixel has no writers" :201
+    kErrStack = 16,     // "gather_stack: offsets leave the clip"           aggregate.cpp:345
+    kErrTopl = 32,      // "top_l: some row has fewer than L valid entries" search.cpp:466
+};
+
+struct Dims {
+    int t, h, w, f;
+    int nh, nw, stride0;
+    int64_t rows;
+};
+
+__host__ __device__ inline Dims make_dims(snls_dims d, int stride0) {
+    Dims r;
+    r.t = d.t;
+    r.h = d.h;
+    r.w = d.w;
+    r.f = d.f;
+    r.stride0 = stride0;
+    r.nh = (d.h - 1) / stride0 + 1;
+    r.nw = (d.w - 1) / stride0 + 1;
+    r.rows = int64_t(d.t) * r.nh * r.nw;
+    return r;
+}
+
+// tensor.cpp:23-29: period-2(n-1) mirror, any magnitude; n == 1 maps to 0.
+__device__ __forceinline__ int reflect(int i, int n) {
+    if (n == 1) return 0;
+    const int period = 2 * (n - 1);
+    int m = i % period;
+    if (m < 0) m += period;
+    return m < n ? m : period - m;
+}
+
+// Cheap reflect for |overshoot| < n (the common case near borders).
+__device__ __forceinline__ int reflect_near(int i, int n) {
+    if (i >= 0 && i < n) return i;
+    return reflect(i, n);
+}
+
+// search.cpp:52-57
+__device__ __forceinline__ void row_coords(const Dims& d, int64_t row, int& qt, int& qy,
+                                           int& qx) {
+    qx = int(row % d.nw) * d.stride0;
+    const int64_t r = row / d.nw;
+    qy = int(r % d.nh) * d.stride0;
+    qt = int(r / d.nh);
+}
+
+// search.cpp:59-68: frame scan order 0, -1, +1, -2, +2, ...
+__host__ __device__ __forceinline__ int scan_dt(int fpos) {
+    return fpos == 0 ? 0 : ((fpos & 1) ? -((fpos + 1) / 2) : fpos / 2);
+}
+
+__device__ __forceinline__ size_t vidx(const Dims& d, int t, int y, int x) {
+    return ((size_t(t) * d.h + y) * d.w + x) * size_t(d.f);
+}
+
+// Bilinear taps of a fractional position (tensor.cpp:31-48) split as integer base +
+// fp32 fraction; weights from the raw (unreflected) position.
+struct Taps {
+    int y0, y1, x0, x1;
+    float w00, w01, w10, w11, fy, fx;
+};
+
+__device__ __forceinline__ Taps taps_from(int by, float fy, int bx, float fx, int h, int w) {
+    Taps t;
+    t.fy = fy;
+    t.fx = fx;
+    t.y0 = reflect_near(by, h);
+    t.y1 = reflect_near(by + 1, h);
+    t.x0 = reflect_near(bx, w);
+    t.x1 = reflect_near(bx + 1, w);
+    t.w00 = (1.f - fy) * (1.f - fx);
+    t.w01 = (1.f - fy) * fx;
+    t.w10 = fy * (1.f - fx);
+    t.w11 = fy * fx;
+    return t;
+}
+
+// Position given in fp64 (absolute coordinate).
+__device__ __forceinline__ Taps taps_at(double y, double x, int h, int w) {
+    const double by = floor(y), bx = floor(x);
+    return taps_from(int(by), float(y - by), int(bx), float(x - bx), h, w);
+}
+
+// Position = integer `base` + fp32 `off` (off may be any magnitude that fp32 holds).
+__device__ __forceinline__ void split_pos(int base, float off, int& ib, float& fr) {
+    const float fl = floorf(off);
+    ib = base + int(fl);
+    fr = off - fl;  // exact (Sterbenz) for |off| >= 1 and for 0 <= off < 1
+}
+
+__device__ __forceinline__ float blend(const Taps& t, float a, float b, float c, float d) {
+    return t.w00 * a + t.w01 * b + t.w10 * c + t.w11 * d;
+}
+
+// search.cpp:72-122 on device: the window shift to frame qt + dt in fp64.  dt == 0 reads
+// the forward field at the query pixel; |dt| >= 1 sums per-step fields, later links
+// bilinear-sampled at the displaced position.  `links` (optional) receives |dt|-1 links of
+// (pos_y - qy, pos_x - qx, J00, J01, J10, J11).
+__device__ inline void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
+                                int h, int w, int qt, int qy, int qx, int dt, double& dy,
+                                double& dx, float* links) {
+    if (ff == nullptr) {  // nls_forward: zero flows
+        dy = 0.0;
+        dx = 0.0;
+        if (links)
+            for (int k = 1; k < (dt < 0 ? -dt : dt); ++k)
+                for (int j = 0; j < 6; ++j) links[(k - 1) * 6 + j] = 0.f;
+        return;
+    }
+    auto at = [&](const float* fl, int t, int y, int x, int c) {
+        return double(__ldg(fl + ((size_t(t) * h + y) * w + x) * 2 + c));
+    };
+    if (dt == 0) {
+        dy = at(ff, qt, qy, qx, 0);
+        dx = at(ff, qt, qy, qx, 1);
+        return;
+    }
+    const float* fld = dt > 0 ? ff : bf;
+    const int step = dt > 0 ? 1 : -1;
+    const int m = dt > 0 ? dt : -dt;
+    double sy = 0.0, sx = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const int fr = qt + step * k;
+        double vy, vx;
+        if (k == 0) {
+            vy = at(fld, fr, qy, qx, 0);
+            vx = at(fld, fr, qy, qx, 1);
+        } else {
+            const double py = double(qy) + sy, px = double(qx) + sx;
+            const double fby = floor(py), fbx = floor(px);
+            const double fy = py - fby, fx = px - fbx;
+            const int y0 = reflect_near(int(fby), h), y1 = reflect_near(int(fby) + 1, h);
+            const int x0 = reflect_near(int(fbx), w), x1 = reflect_near(int(fbx) + 1, w);
+            const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);
+            const double cy = at(fld, fr, y1, x0, 0), dyv = at(fld, fr, y1, x1, 0);
+            const double ax = at(fld, fr, y0, x0, 1), bx = at(fld, fr, y0, x1, 1);
+            const double cx = at(fld, fr, y1, x0, 1), dxv = at(fld, fr, y1, x1, 1);
+            const double w00 = (1.0 - fy) * (1.0 - fx), w01 = (1.0 - fy) * fx;
+            const double w10 = fy * (1.0 - fx), w11 = fy * fx;
+            vy = w00 * ay + w01 * by + w10 * cy + w11 * dyv;
+            vx = w00 * ax + w01 * bx + w10 * cx + w11 * dxv;
+            if (links) {
+                float* lk = links + (k - 1) * 6;
+                lk[0] = float(sy);
+                lk[1] = float(sx);
+                lk[2] = float(-(1.0 - fx) * ay - fx * by + (1.0 - fx) * cy + fx * dyv);
+                lk[3] = float(-(1.0 - fy) * ay + (1.0 - fy) * by - fy * cy + fy * dyv);
+                lk[4] = float(-(1.0 - fx) * ax - fx * bx + (1.0 - fx) * cx + fx * dxv);
+                lk[5] = float(-(1.0 - fy) * ax + (1.0 - fy) * bx - fy * cx + fy * dxv);
+            }
+        }
+        sy += vy;
+        sx += vx;
+    }
+    dy = sy;
+    dx = sx;
+}
+
+// Total order used for top-L: value descending, then slot ascending (search.cpp:187-197,
+// 390-393).  Packed into one u64 so a warp max-reduction is a single comparison chain.
+__device__ __forceinline__ uint32_t orderable(float v) {
+    const uint32_t b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_orderable(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+__device__ __forceinline__ uint64_t pack_key(float v, uint32_t slot) {
+    return (uint64_t(orderable(v)) << 32) | uint64_t(0xffffffffu - slot);
+}
+__device__ __forceinline__ uint32_t key_slot(uint64_t k) {
+    return 0xffffffffu - uint32_t(k & 0xffffffffu);
+}
+__device__ __forceinline__ float key_value(uint64_t k) { return from_orderable(uint32_t(k >> 32)); }
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+
+// A candidate is eligible for top-L only if it compares greater than -inf (NaN and -inf
+// never enter, search.cpp:188).
+__device__ __forceinline__ bool eligible(float v) { return v > -INFINITY; }
+
+__device__ __forceinline__ void latch(int* err, int bit) {
+    if (err) atomicOr(err, bit);
+}
+
+}  // namespace snls_gpu

@@ -1,0 +1,68 @@
+// Host-side launch interface between the C-ABI (capi.cu) and the kernel translation units.
+// Launchers return 1 when they enqueued a kernel, 0 when nothing was needed, and -1 when
+// the configuration cannot be served (the caller maps that to a status).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace snls_gpu {
+
+struct GenericSearch {
+    const float *q, *k, *ff, *bf;
+    Dims d;
+    int ws, wt, ps, topl, metric;
+    double stride1;
+    float beta;
+    float *sims, *offsets, *chains, *weights;
+    float *grid, *grid_offsets;
+    int select;
+    int* err;
+};
+
+struct TiledSearch {
+    const float *q, *k, *ff, *bf;
+    Dims d;
+    int ws, wt, ps, topl, metric;
+    float beta;
+    float *sims, *offsets, *chains, *weights;
+    int* err;
+    int num_sms;
+};
+
+struct AggArgs {
+    const float* v;
+    const float* weights;
+    const float* offsets;
+    Dims d;
+    int ps, topl;
+    int* err;
+};
+
+int launch_flows_check(const float* ff, const float* bf, int64_t n, int* err, cudaStream_t st);
+int launch_search_generic(const GenericSearch& g, cudaStream_t st);
+// Returns 0 when (ws, ps, f, topl) has no tiled instantiation (caller falls back).
+int launch_search_tiled(const TiledSearch& s, cudaStream_t st);
+int launch_topl(int64_t rows, int cols, const float* full, const float* full_offsets, int topl,
+                float* sel, float* sel_offsets, int* err, cudaStream_t st);
+int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,
+                     const float* offsets, float* chains, cudaStream_t st);
+int launch_replay(const float* q, const float* k, Dims d, int ps, int metric, int topl,
+                  const float* offsets, float* sims, cudaStream_t st);
+
+int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* weights, int* err,
+                   cudaStream_t st);
+int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st);
+int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st);
+int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
+                     float* dw, cudaStream_t st);
+
+// `gyx`: rows * topl * 2 doubles of zeroed scratch.  Returns the number of launches.
+int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
+                           const float* q, const float* k, Dims d, int wt, int ps, int topl,
+                           int metric, float* dq, float* dk, float* dff, float* dbf, double* gyx,
+                           cudaStream_t st);
+
+}  // namespace snls_gpu

@@ -1,0 +1,152 @@
+// Search backward (shifted_nls_backward, search.cpp:499-711) on device.
+//
+// Phase 1: one thread per (selected entry, channel group).  It replays the entry's patch
+// (same taps as the forward), scatters dQ into the reflected query pixels and dK into the
+// 4 bilinear taps with atomics, and accumulates its share of dS/d(ky, kx) in fp64.  The
+// per-entry (gy, gx) is reduced across the channel-group threads with fp64 atomics.
+// Phase 2: one thread per entry routes (gy, gx) back through the composition chain
+// (search.cpp:584-666): dt >= 0 into dFflow, dt < 0 into dBflow, v <- (I + J)^T v per link.
+// Entries with a zero upstream gradient are skipped (search.cpp:692).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace snls_gpu {
+
+namespace {
+
+template <int VEC>
+__global__ void __launch_bounds__(256) search_bwd_entries(const float* __restrict__ grad,
+                                                          const float* __restrict__ offsets,
+                                                          const float* __restrict__ q,
+                                                          const float* __restrict__ k, Dims d,
+                                                          int ps, int topl, int metric,
+                                                          float* dq, float* dk, double* gyx) {
+    const int groups = d.f / VEC;
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= d.rows * topl * groups) return;
+    const int64_t e = idx / groups;
+    const int c = int(idx % groups) * VEC;
+    const float g = grad[e];
+    if (g == 0.f) return;
+    const int64_t row = e / topl;
+    int qt, qy, qx;
+    row_coords(d, row, qt, qy, qx);
+    const float* o = offsets + size_t(e) * 3;
+    const int kt = qt + int(rintf(o[0]));
+    const float oy = o[1], ox = o[2];
+    const int half = ps / 2;
+    double gy = 0.0, gx = 0.0;
+    for (int py = -half; py <= half; ++py) {
+        const int ry = reflect_near(qy + py, d.h);
+        for (int px = -half; px <= half; ++px) {
+            const int rx = reflect_near(qx + px, d.w);
+            int iy, ix;
+            float fy, fx;
+            split_pos(qy + py, oy, iy, fy);
+            split_pos(qx + px, ox, ix, fx);
+            const Taps t = taps_from(iy, fy, ix, fx, d.h, d.w);
+            const size_t iq = vidx(d, qt, ry, rx) + c;
+            const size_t i00 = vidx(d, kt, t.y0, t.x0) + c, i01 = vidx(d, kt, t.y0, t.x1) + c;
+            const size_t i10 = vidx(d, kt, t.y1, t.x0) + c, i11 = vidx(d, kt, t.y1, t.x1) + c;
+            float sy = 0.f, sx = 0.f;
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+                const float qv = __ldg(q + iq + j);
+                const float k00 = __ldg(k + i00 + j), k01 = __ldg(k + i01 + j);
+                const float k10 = __ldg(k + i10 + j), k11 = __ldg(k + i11 + j);
+                const float kv = blend(t, k00, k01, k10, k11);
+                float ds_dq, ds_dk;
+                if (metric == SNLS_METRIC_IP) {
+                    ds_dq = kv;
+                    ds_dk = qv;
+                } else {
+                    const float diff = qv - kv;
+                    ds_dq = -2.f * diff;
+                    ds_dk = 2.f * diff;
+                }
+                const float gq = g * ds_dq, gk = g * ds_dk;
+                atomicAdd(dq + iq + j, gq);
+                atomicAdd(dk + i00 + j, gk * t.w00);
+                atomicAdd(dk + i01 + j, gk * t.w01);
+                atomicAdd(dk + i10 + j, gk * t.w10);
+                atomicAdd(dk + i11 + j, gk * t.w11);
+                // d(sample)/dy, d(sample)/dx from the tap values (search.cpp:574-577)
+                const float dkv_dy = (1.f - fx) * (k10 - k00) + fx * (k11 - k01);
+                const float dkv_dx = (1.f - fy) * (k01 - k00) + fy * (k11 - k10);
+                sy = fmaf(gk, dkv_dy, sy);
+                sx = fmaf(gk, dkv_dx, sx);
+            }
+            gy += double(sy);
+            gx += double(sx);
+        }
+    }
+    atomicAdd(gyx + 2 * e, gy);
+    atomicAdd(gyx + 2 * e + 1, gx);
+}
+
+__global__ void search_bwd_route(const float* __restrict__ grad,
+                                 const float* __restrict__ offsets,
+                                 const float* __restrict__ chains, Dims d, int wt, int topl,
+                                 const double* __restrict__ gyx, float* dff, float* dbf) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= d.rows * topl) return;
+    if (grad[e] == 0.f) return;
+    const int64_t row = e / topl;
+    int qt, qy, qx;
+    row_coords(d, row, qt, qy, qx);
+    const int dt = int(rintf(offsets[size_t(e) * 3]));
+    float* fld = dt >= 0 ? dff : dbf;
+    const int step = dt >= 0 ? 1 : -1;
+    const int m = dt == 0 ? 1 : (dt > 0 ? dt : -dt);
+    double vy = gyx[2 * e], vx = gyx[2 * e + 1];
+    const int cs = wt > 1 ? wt - 1 : 0;
+    const float* chain = chains ? chains + size_t(e) * cs * 6 : nullptr;
+    for (int kk = m - 1; kk >= 1; --kk) {
+        const float* lk = chain + (kk - 1) * 6;
+        int iy, ix;
+        float fy, fx;
+        split_pos(qy, lk[0], iy, fy);
+        split_pos(qx, lk[1], ix, fx);
+        const Taps t = taps_from(iy, fy, ix, fx, d.h, d.w);
+        const int fr = qt + step * kk;
+        auto at = [&](int y, int x, int comp) { return fld + ((size_t(fr) * d.h + y) * d.w + x) * 2 + comp; };
+        atomicAdd(at(t.y0, t.x0, 0), float(vy * t.w00));
+        atomicAdd(at(t.y0, t.x1, 0), float(vy * t.w01));
+        atomicAdd(at(t.y1, t.x0, 0), float(vy * t.w10));
+        atomicAdd(at(t.y1, t.x1, 0), float(vy * t.w11));
+        atomicAdd(at(t.y0, t.x0, 1), float(vx * t.w00));
+        atomicAdd(at(t.y0, t.x1, 1), float(vx * t.w01));
+        atomicAdd(at(t.y1, t.x0, 1), float(vx * t.w10));
+        atomicAdd(at(t.y1, t.x1, 1), float(vx * t.w11));
+        const double ny = vy + double(lk[2]) * vy + double(lk[4]) * vx;
+        const double nx = vx + double(lk[3]) * vy + double(lk[5]) * vx;
+        vy = ny;
+        vx = nx;
+    }
+    float* base = fld + ((size_t(qt) * d.h + qy) * d.w + qx) * 2;
+    atomicAdd(base, float(vy));
+    atomicAdd(base + 1, float(vx));
+}
+
+}  // namespace
+
+// `gyx` scratch: rows * topl * 2 doubles, zeroed by the caller.
+int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
+                           const float* q, const float* k, Dims d, int wt, int ps, int topl,
+                           int metric, float* dq, float* dk, float* dff, float* dbf, double* gyx,
+                           cudaStream_t st) {
+    const int vec = d.f % 4 == 0 ? 4 : 1;
+    const int64_t n = d.rows * topl * (d.f / vec);
+    if (vec == 4)
+        search_bwd_entries<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps,
+                                                                         topl, metric, dq, dk, gyx);
+    else
+        search_bwd_entries<1><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps,
+                                                                         topl, metric, dq, dk, gyx);
+    const int64_t ne = d.rows * topl;
+    search_bwd_route<<<unsigned((ne + 255) / 256), 256, 0, st>>>(grad, offsets, chains, d, wt, topl,
+                                                                 gyx, dff, dbf);
+    return 2;
+}
+
+}  // namespace snls_gpu

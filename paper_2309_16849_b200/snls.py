@@ -1,0 +1,448 @@
+"""Python front end over the C-ABI (include/snls_cuda.h) -- the same operator surface as the
+reference's C++ API (search.hpp:126-158, aggregate.hpp:22-85), on torch CUDA tensors.
+
+torch is only the device-memory / stream plumbing here: every operation is one or more of
+the hand-written sm_100a kernels in libsnls_cuda.so, called through ctypes.  There is no
+CPU fallback: if the library or a B200 is missing the calls raise.
+
+Error behaviour mirrors the reference: configuration problems raise ConfigError and domain
+problems DomainError (errors.hpp:9-17) with the reference's messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsnls_cuda.so")
+
+METRIC_IP, METRIC_L2 = 0, 1
+MODE_FUSED, MODE_FULLGRID = 0, 1
+
+
+class SnlsError(RuntimeError):
+    pass
+
+
+class ConfigError(SnlsError):
+    """snls::ConfigError (errors.hpp:9-12)."""
+
+
+class DomainError(SnlsError):
+    """snls::DomainError (errors.hpp:14-17)."""
+
+
+class CudaError(SnlsError):
+    pass
+
+
+@dataclass
+class SearchConfig:
+    """snls::SearchConfig (search.hpp:17-35)."""
+
+    ws: int = 9
+    wt: int = 0
+    ps: int = 1
+    stride0: int = 1
+    stride1: float = 1.0
+    topl: int = 1
+    metric: str = "l2"  # 'ip' (inner product) or 'l2' (negated squared L2)
+    softmax_scale: float = 1.0
+
+    def window_frames(self) -> int:
+        return 2 * self.wt + 1
+
+    def window_slots(self) -> int:
+        return self.window_frames() * self.ws * self.ws
+
+    def hole_free(self) -> bool:
+        return (self.ps - 1) // 2 < self.stride0
+
+    def chain_stride(self) -> int:
+        return max(self.wt - 1, 0)
+
+
+class _Config(C.Structure):
+    _fields_ = [("ws", C.c_int), ("wt", C.c_int), ("ps", C.c_int), ("stride0", C.c_int),
+                ("stride1", C.c_double), ("topl", C.c_int), ("metric", C.c_int),
+                ("softmax_scale", C.c_double)]
+
+
+class _Dims(C.Structure):
+    _fields_ = [("t", C.c_int), ("h", C.c_int), ("w", C.c_int), ("f", C.c_int)]
+
+
+def _cfg(c: SearchConfig) -> _Config:
+    if c.metric not in ("ip", "l2"):
+        raise ConfigError("SearchConfig: unknown metric")
+    return _Config(int(c.ws), int(c.wt), int(c.ps), int(c.stride0), float(c.stride1), int(c.topl),
+                   METRIC_IP if c.metric == "ip" else METRIC_L2, float(c.softmax_scale))
+
+
+_lib = None
+_lib_lock = threading.Lock()
+VOIDP = C.c_void_p
+
+
+def lib() -> C.CDLL:
+    """Load libsnls_cuda.so (raises if it has not been built: no silent fallback)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise CudaError(f"{LIB_PATH} is missing; build it with "
+                                "`python -m paper_2309_16849_b200.build`")
+            L = C.CDLL(LIB_PATH)
+            L.snls_last_error.restype = C.c_char_p
+            L.snls_uniform_fill_f32.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int64, VOIDP]
+            L.snls_query_grid.argtypes = [_Dims, C.c_int, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int), C.POINTER(C.c_int)]
+            L.snls_ctx_create.argtypes = [C.c_int, VOIDP, C.POINTER(VOIDP)]
+            L.snls_ctx_destroy.argtypes = [VOIDP]
+            L.snls_ctx_set_stream.argtypes = [VOIDP, VOIDP]
+            L.snls_ctx_sync_check.argtypes = [VOIDP]
+            L.snls_ctx_launch_count.argtypes = [VOIDP, C.POINTER(C.c_int64)]
+            L.snls_ctx_last_search_path.argtypes = [VOIDP, C.POINTER(C.c_int)]
+            L.snls_ctx_force_generic.argtypes = [VOIDP, C.c_int]
+            L.snls_validate_config.argtypes = [C.POINTER(_Config)]
+            P = C.POINTER(_Config)
+            L.snls_search_fwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, C.c_int,
+                                          VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_search_grid.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_topl.argtypes = [VOIDP, C.c_int64, C.c_int, VOIDP, VOIDP, C.c_int, VOIDP, VOIDP]
+            L.snls_replay.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_search_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
+                                          VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_softmax_rows.argtypes = [VOIDP, C.c_int64, C.c_int, C.c_double, VOIDP, VOIDP]
+            L.snls_wpsum_fwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_gather_stack.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_wpsum_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
+                                         VOIDP, VOIDP]
+            _lib = L
+        return _lib
+
+
+def _raise(rc: int):
+    if rc == 0:
+        return
+    msg = lib().snls_last_error().decode()
+    if rc == 1:
+        raise ConfigError(msg)
+    if rc == 2:
+        raise DomainError(msg)
+    if rc == 3:
+        raise CudaError(msg)
+    raise SnlsError(msg)
+
+
+def validate(cfg: SearchConfig) -> None:
+    """SearchConfig::validate (search.cpp:21-32) -- host only, no device needed."""
+    c = _cfg(cfg)
+    _raise(lib().snls_validate_config(C.byref(c)))
+
+
+def query_grid(t: int, h: int, w: int, stride0: int):
+    rows, nh, nw = C.c_int64(), C.c_int(), C.c_int()
+    _raise(lib().snls_query_grid(_Dims(t, h, w, 1), stride0, C.byref(rows), C.byref(nh), C.byref(nw)))
+    return rows.value, nh.value, nw.value
+
+
+def uniform_fill(seed: int, lo: float, hi: float, n: int):
+    """UniformStream(seed).next_in(lo, hi) (rng.hpp:12-24) as float32 numpy, host side."""
+    import numpy as np
+
+    out = np.empty(n, np.float32)
+    _raise(lib().snls_uniform_fill_f32(C.c_uint64(seed), lo, hi, n, out.ctypes.data))
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+class Context:
+    """One snls_ctx per (device, stream)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+
+        self.torch = torch
+        self.device = device
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.stream = s
+        h = VOIDP()
+        _raise(lib().snls_ctx_create(device, VOIDP(s.cuda_stream), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().snls_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        self.stream = stream
+        _raise(lib().snls_ctx_set_stream(self.h, VOIDP(stream.cuda_stream)))
+
+    def sync_check(self):
+        _raise(lib().snls_ctx_sync_check(self.h))
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _raise(lib().snls_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def last_search_path(self) -> int:
+        n = C.c_int()
+        _raise(lib().snls_ctx_last_search_path(self.h, C.byref(n)))
+        return n.value
+
+    def force_generic(self, on: bool):
+        _raise(lib().snls_ctx_force_generic(self.h, int(on)))
+
+
+_ctxs: dict = {}
+
+
+def context(device: Optional[int] = None) -> Context:
+    import torch
+
+    dev = torch.cuda.current_device() if device is None else device
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    if key not in _ctxs:
+        _ctxs[key] = Context(dev, torch.cuda.current_stream(dev))
+    return _ctxs[key]
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    import torch
+
+    if not t.is_cuda:
+        raise SnlsError("snls: tensors must live on a CUDA device")
+    if not t.is_contiguous():
+        raise SnlsError("snls: tensors must be contiguous")
+    if t.dtype not in (torch.float32, torch.int32):
+        raise SnlsError(f"snls: unsupported dtype {t.dtype}")
+    return VOIDP(t.data_ptr())
+
+
+def _dims(v) -> _Dims:
+    if v.dim() != 4:
+        raise DomainError("snls: videos are T x H x W x F")
+    t, h, w, f = v.shape
+    return _Dims(t, h, w, f)
+
+
+@dataclass
+class SearchResult:
+    """snls::SearchResult (search.hpp:112-116) with the device tape (see snls_cuda.h)."""
+
+    sims: object
+    offsets: object
+    chains: object = None
+    weights: object = None
+    cfg: SearchConfig = field(default_factory=SearchConfig)
+
+    def centers(self):
+        """Absolute key centres (kt, ky, kx) of the reference tape, as float64."""
+        import torch
+
+        rows = self.sims.shape[0]
+        t, nh, nw = self._grid
+        s0 = self.cfg.stride0
+        r = torch.arange(rows, device=self.sims.device)
+        qx = (r % nw) * s0
+        qy = ((r // nw) % nh) * s0
+        qt = r // (nw * nh)
+        base = torch.stack([qt, qy, qx], -1).double()[:, None, :]
+        return base + self.offsets.double()
+
+
+def shifted_nls_forward(q, k, fflow, bflow, cfg: SearchConfig, mode: int = MODE_FUSED,
+                        want_chains: bool = True, want_weights: bool = False,
+                        ctx: Optional[Context] = None, check: bool = True, out=None) -> SearchResult:
+    """snls::shifted_nls_forward (search.hpp:126-128). fflow/bflow None => nls_forward."""
+    import torch
+
+    ctx = ctx or context(q.device.index)
+    t, h, w, f = q.shape
+    if tuple(k.shape) != tuple(q.shape):
+        raise DomainError("search: query and key shapes differ")
+    if fflow is not None and (tuple(fflow.shape) != (t, h, w, 2) or tuple(bflow.shape) != (t, h, w, 2)):
+        raise DomainError("search: flow shape does not match the video")
+    c = _cfg(cfg)
+    _raise(lib().snls_validate_config(C.byref(c)))
+    rows = t * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    if out is None:
+        sims = torch.empty((rows, cfg.topl), device=q.device, dtype=torch.float32)
+        offs = torch.empty((rows, cfg.topl, 3), device=q.device, dtype=torch.float32)
+        chains = (torch.empty((rows, cfg.topl, cfg.chain_stride(), 6), device=q.device,
+                              dtype=torch.float32) if want_chains and cfg.wt > 1 else None)
+        weights = (torch.empty((rows, cfg.topl), device=q.device, dtype=torch.float32)
+                   if want_weights else None)
+    else:
+        sims, offs, chains, weights = out
+    _raise(lib().snls_search_fwd(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(fflow),
+                                 _ptr(bflow), int(mode), _ptr(sims), _ptr(offs), _ptr(chains),
+                                 _ptr(weights)))
+    if check:
+        ctx.sync_check()
+    res = SearchResult(sims, offs, chains, weights, cfg)
+    res._grid = (t, (h - 1) // cfg.stride0 + 1, (w - 1) // cfg.stride0 + 1)
+    return res
+
+
+def nls_forward(q, k, cfg: SearchConfig, **kw) -> SearchResult:
+    """snls::nls_forward (search.hpp:131-132): both flows identically zero."""
+    return shifted_nls_forward(q, k, None, None, cfg, **kw)
+
+
+def search_grid(q, k, fflow, bflow, cfg: SearchConfig, ctx=None):
+    """Materialised pre-selection grid (full_grid_forward, search.cpp:351-376)."""
+    import torch
+
+    ctx = ctx or context(q.device.index)
+    t, h, w, f = q.shape
+    c = _cfg(cfg)
+    rows = t * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    n = cfg.window_slots()
+    grid = torch.empty((rows, n), device=q.device, dtype=torch.float32)
+    goff = torch.empty((rows, n, 3), device=q.device, dtype=torch.float32)
+    _raise(lib().snls_search_grid(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(fflow),
+                                  _ptr(bflow), _ptr(grid), _ptr(goff)))
+    ctx.sync_check()
+    return grid, goff
+
+
+def top_l(full, full_offsets, topl: int, ctx=None):
+    """snls::top_l (search.hpp:137-138)."""
+    import torch
+
+    ctx = ctx or context(full.device.index)
+    rows, cols = full.shape
+    if tuple(full_offsets.shape) != (rows, cols, 3):
+        raise DomainError("top_l: similarity and offset shapes disagree")
+    sel = torch.empty((rows, max(topl, 1)), device=full.device, dtype=torch.float32)
+    soff = torch.empty((rows, max(topl, 1), 3), device=full.device, dtype=torch.float32)
+    _raise(lib().snls_topl(ctx.h, rows, cols, _ptr(full), _ptr(full_offsets), int(topl),
+                           _ptr(sel), _ptr(soff)))
+    ctx.sync_check()
+    return sel, soff
+
+
+def replay_similarities(res: SearchResult, q, k, ctx=None):
+    """snls::replay_similarities (search.hpp:157-158), from the device tape."""
+    import torch
+
+    ctx = ctx or context(q.device.index)
+    c = _cfg(res.cfg)
+    sims = torch.empty_like(res.sims)
+    _raise(lib().snls_replay(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(res.offsets),
+                             _ptr(sims)))
+    ctx.sync_check()
+    return sims
+
+
+def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=True):
+    """snls::shifted_nls_backward (search.hpp:151-153) -> (dq, dk, dfflow, dbflow)."""
+    import torch
+
+    ctx = ctx or context(q.device.index)
+    c = _cfg(res.cfg)
+    t, h, w, f = q.shape
+    if tuple(grad_sims.shape) != tuple(res.sims.shape):
+        raise DomainError("shifted_nls_backward: gradient shape does not match the tape")
+    dq = torch.empty_like(q)
+    dk = torch.empty_like(q)
+    dff = torch.empty((t, h, w, 2), device=q.device, dtype=torch.float32)
+    dbf = torch.empty_like(dff)
+    _raise(lib().snls_search_bwd(ctx.h, C.byref(c), _dims(q), _ptr(grad_sims), _ptr(res.offsets),
+                                 _ptr(res.chains), _ptr(q), _ptr(k), _ptr(dq), _ptr(dk), _ptr(dff),
+                                 _ptr(dbf)))
+    if check:
+        ctx.sync_check()
+    return dq, dk, dff, dbf
+
+
+def softmax_rows(sims, beta: float, ctx=None, check=True):
+    """snls::softmax_rows (aggregate.hpp:22)."""
+    import torch
+
+    ctx = ctx or context(sims.device.index)
+    rows, l = sims.shape
+    w = torch.empty_like(sims)
+    _raise(lib().snls_softmax_rows(ctx.h, rows, l, float(beta), _ptr(sims), _ptr(w)))
+    if check:
+        ctx.sync_check()
+    return w
+
+
+def _agg_shape_checks(v, weights, offsets, cfg):
+    t, h, w, f = v.shape
+    rows = t * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    validate(cfg)
+    if not cfg.hole_free():
+        raise ConfigError("aggregate: (ps-1)/2 < stride0 is required for hole-free output")
+    if weights.shape[0] != rows or offsets.shape[0] != rows:
+        raise DomainError("aggregate: weight/offset rows do not match the query grid")
+    if weights.shape[1] != offsets.shape[1] or weights.shape[1] != cfg.topl:
+        raise DomainError("aggregate: weight/offset L does not match the config")
+
+
+def wpsum(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True, out=None):
+    """snls::wpsum (aggregate.hpp:53-54) -> (video, counts)."""
+    import torch
+
+    ctx = ctx or context(v.device.index)
+    _agg_shape_checks(v, weights, offsets, cfg)
+    c = _cfg(cfg)
+    t, h, w, f = v.shape
+    if out is None:
+        o = torch.empty_like(v)
+        counts = torch.empty((t, h, w), device=v.device, dtype=torch.int32)
+    else:
+        o, counts = out
+    _raise(lib().snls_wpsum_fwd(ctx.h, C.byref(c), _dims(v), _ptr(v), _ptr(weights), _ptr(offsets),
+                                _ptr(o), _ptr(counts)))
+    if check:
+        ctx.sync_check()
+    return o, counts
+
+
+def gather_stack(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True):
+    """snls::gather_stack (aggregate.hpp:71-73) -> L x T x H x W x F."""
+    import torch
+
+    ctx = ctx or context(v.device.index)
+    _agg_shape_checks(v, weights, offsets, cfg)
+    c = _cfg(cfg)
+    out = torch.empty((cfg.topl, *v.shape), device=v.device, dtype=torch.float32)
+    _raise(lib().snls_gather_stack(ctx.h, C.byref(c), _dims(v), _ptr(v), _ptr(weights),
+                                   _ptr(offsets), _ptr(out)))
+    if check:
+        ctx.sync_check()
+    return out
+
+
+def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx=None, check=True):
+    """snls::wpsum_backward (aggregate.hpp:83-85) -> (dv, dweights)."""
+    import torch
+
+    ctx = ctx or context(v.device.index)
+    if tuple(grad_out.shape) != tuple(v.shape):
+        raise DomainError("wpsum_backward: gradient shape does not match the tape")
+    c = _cfg(cfg)
+    dv = torch.empty_like(v)
+    dw = torch.empty_like(weights)
+    _raise(lib().snls_wpsum_bwd(ctx.h, C.byref(c), _dims(v), _ptr(grad_out), _ptr(counts), _ptr(v),
+                                _ptr(weights), _ptr(offsets), _ptr(dv), _ptr(dw)))
+    if check:
+        ctx.sync_check()
+    return dv, dw

@@ -368,9 +368,7 @@ int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const
     const size_t nv = size_t(dims.t) * dims.h * dims.w;
     cudaMemsetAsync(dq, 0, nv * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
-    cudaMemsetAsync(dff, 0, nv * 2 * sizeof(float), ctx->stream);
-    cudaMemsetAsync(dbf, 0, nv * 2 * sizeof(float), ctx->stream);
-    const size_t scratch = size_t(d.rows) * cfg->topl * 2 * sizeof(double);
+    const size_t scratch = (size_t(d.rows) * cfg->topl * 2 + nv * 4) * sizeof(double);
     if (int rc = ensure_work(ctx, scratch)) return rc;
     cudaMemsetAsync(ctx->work, 0, scratch, ctx->stream);
     const int n = launch_search_bwd_impl(grad, offsets, chains, q, k, d, cfg->wt, cfg->ps, cfg->topl,

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 __global__ void search_bwd_route(const float* __restrict__ grad,
                                  const float* __restrict__ offsets,
                                  const float* __restrict__ chains, Dims d, int wt, int topl,
-                                 const double* __restrict__ gyx, float* dff, float* dbf) {
+                                 const double* __restrict__ gyx, double* dff, double* dbf) {
     const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= d.rows * topl) return;
     if (grad[e] == 0.f) return;
@@ -95,7 +95,7 @@ __global__ void search_bwd_route(const float* __restrict__ grad,
     int qt, qy, qx;
     row_coords(d, row, qt, qy, qx);
     const int dt = int(rintf(offsets[size_t(e) * 3]));
-    float* fld = dt >= 0 ? dff : dbf;
+    double* fld = dt >= 0 ? dff : dbf;
     const int step = dt >= 0 ? 1 : -1;
     const int m = dt == 0 ? 1 : (dt > 0 ? dt : -dt);
     double vy = gyx[2 * e], vx = gyx[2 * e + 1];
@@ -110,31 +110,45 @@ __global__ void search_bwd_route(const float* __restrict__ grad,
         const Taps t = taps_from(iy, fy, ix, fx, d.h, d.w);
         const int fr = qt + step * kk;
         auto at = [&](int y, int x, int comp) { return fld + ((size_t(fr) * d.h + y) * d.w + x) * 2 + comp; };
-        atomicAdd(at(t.y0, t.x0, 0), float(vy * t.w00));
-        atomicAdd(at(t.y0, t.x1, 0), float(vy * t.w01));
-        atomicAdd(at(t.y1, t.x0, 0), float(vy * t.w10));
-        atomicAdd(at(t.y1, t.x1, 0), float(vy * t.w11));
-        atomicAdd(at(t.y0, t.x0, 1), float(vx * t.w00));
-        atomicAdd(at(t.y0, t.x1, 1), float(vx * t.w01));
-        atomicAdd(at(t.y1, t.x0, 1), float(vx * t.w10));
-        atomicAdd(at(t.y1, t.x1, 1), float(vx * t.w11));
+        atomicAdd(at(t.y0, t.x0, 0), vy * t.w00);
+        atomicAdd(at(t.y0, t.x1, 0), vy * t.w01);
+        atomicAdd(at(t.y1, t.x0, 0), vy * t.w10);
+        atomicAdd(at(t.y1, t.x1, 0), vy * t.w11);
+        atomicAdd(at(t.y0, t.x0, 1), vx * t.w00);
+        atomicAdd(at(t.y0, t.x1, 1), vx * t.w01);
+        atomicAdd(at(t.y1, t.x0, 1), vx * t.w10);
+        atomicAdd(at(t.y1, t.x1, 1), vx * t.w11);
         const double ny = vy + double(lk[2]) * vy + double(lk[4]) * vx;
         const double nx = vx + double(lk[3]) * vy + double(lk[5]) * vx;
         vy = ny;
         vx = nx;
     }
-    float* base = fld + ((size_t(qt) * d.h + qy) * d.w + qx) * 2;
-    atomicAdd(base, float(vy));
-    atomicAdd(base + 1, float(vx));
+    double* base = fld + ((size_t(qt) * d.h + qy) * d.w + qx) * 2;
+    atomicAdd(base, vy);
+    atomicAdd(base + 1, vx);
+}
+
+__global__ void narrow_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                              float* __restrict__ fa, float* __restrict__ fb, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        fa[i] = float(a[i]);
+        fb[i] = float(b[i]);
+    }
 }
 
 }  // namespace
 
-// `gyx` scratch: rows * topl * 2 doubles, zeroed by the caller.
+// `gyx` scratch: rows * topl * 2 doubles, then two fp64 flow-gradient accumulators of
+// T*H*W*2 doubles each (the flow gradient sums many cancelling terms: fp64 atomics, then
+// one narrowing pass), all zeroed by the caller.
 int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
                            const float* q, const float* k, Dims d, int wt, int ps, int topl,
                            int metric, float* dq, float* dk, float* dff, float* dbf, double* gyx,
                            cudaStream_t st) {
+    double* dff64 = gyx + size_t(d.rows) * topl * 2;
+    const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
+    double* dbf64 = dff64 + nfl;
     const int vec = d.f % 4 == 0 ? 4 : 1;
     const int64_t n = d.rows * topl * (d.f / vec);
     if (vec == 4)
@@ -145,8 +159,10 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
                                                                          topl, metric, dq, dk, gyx);
     const int64_t ne = d.rows * topl;
     search_bwd_route<<<unsigned((ne + 255) / 256), 256, 0, st>>>(grad, offsets, chains, d, wt, topl,
-                                                                 gyx, dff, dbf);
-    return 2;
+                                                                 gyx, dff64, dbf64);
+    narrow_kernel<<<unsigned(std::min<int64_t>((nfl + 255) / 256, 4096)), 256, 0, st>>>(dff64, dbf64, dff,
+                                                                                       dbf, nfl);
+    return 3;
 }
 
 }  // namespace snls_gpu

@@ -308,6 +308,8 @@ int launch_cfg(const TiledSearch& s, cudaStream_t st) {
 template <int P, int W, int KMAX>
 int launch_by_f(const TiledSearch& s, cudaStream_t st) {
     switch (s.d.f) {
+        case 4: return launch_cfg<P, W, 4, 1, KMAX>(s, st);
+        case 8: return launch_cfg<P, W, 4, 2, KMAX>(s, st);
         case 16: return launch_cfg<P, W, 4, 4, KMAX>(s, st);
         case 32: return launch_cfg<P, W, 4, 8, KMAX>(s, st);
         case 64: return launch_cfg<P, W, 4, 16, KMAX>(s, st);

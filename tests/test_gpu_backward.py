@@ -23,7 +23,7 @@ def gpu_bwd(q, k, cfg, offsets, chains_abs, grad):
     S = snls_mod()
     t, h, w, _ = q.shape
     res = S.SearchResult(sims=dev(np.zeros(offsets.shape[:2])), offsets=dev(offsets),
-                         chains=dev(rel_chains(chains_abs, cfg, t, h, w)) if cfg.wt > 1 else None,
+                         chains=dev(rel_chains(chains_abs, cfg, t, h, w, offsets)) if cfg.wt > 1 else None,
                          cfg=scfg(cfg))
     return [host(x) for x in S.shifted_nls_backward(dev(grad), res, dev(q), dev(k))]
 

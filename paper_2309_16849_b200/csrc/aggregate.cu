@@ -150,6 +150,200 @@ __global__ void __launch_bounds__(256) gather_stack_kernel(AggArgs a, float* __r
         o[0] = acc[0];
 }
 
+// ---- tiled gather -----------------------------------------------------------------------
+// A CTA owns a run of PPC consecutive output pixels of one row (t, y) and all channels
+// (G = F/4 lanes per pixel, float4 each).  Phase 1 turns every (query, neighbour) that can
+// write into the run into a sample descriptor in shared memory: frame, integer offset and
+// the four bilinear weights pre-multiplied by the softmax weight.  Phase 2 is the
+// reference's fixed-order gather (footprint py/px ascending, then the owning query's cell
+// completion; neighbours ascending), each unit costing 2 LDS + 4 coalesced LDG.128 + 16 FFMA
+// per lane instead of re-deriving taps from the offsets in every channel lane.
+struct SampleDesc {
+    int kt, oy, ox, ok;
+    float w00, w01, w10, w11;
+};
+
+struct TileGeom {
+    int gy_lo, nqy, gx_lo, nqx;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const AggArgs& a, int y, int x0, int ppc) {
+    const int st = a.d.stride0;
+    TileGeom g;
+    // any query writing pixel y lies within s0-1 rows of it (footprint: half < s0; cell
+    // completion: the owner, possibly clamped to the last grid row)
+    const int lo_y = max(0, (y - (st - 1) + st - 1) / st - 1);
+    const int hi_y = min(a.d.nh - 1, (y + st - 1) / st);
+    g.gy_lo = max(0, lo_y);
+    g.nqy = hi_y - g.gy_lo + 1;
+    const int x1 = min(x0 + ppc, a.d.w) - 1;
+    g.gx_lo = max(0, (x0 - (st - 1)) / st - 1);
+    const int hi_x = min(a.d.nw - 1, (x1 + st - 1) / st);
+    g.nqx = hi_x - g.gx_lo + 1;
+    return g;
+}
+
+__device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleDesc* desc,
+                            int* err_bit, int err_code) {
+    const int n = g.nqy * g.nqx * a.topl;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i % a.topl, qi = i / a.topl;
+        const int gy = g.gy_lo + qi / g.nqx, gx = g.gx_lo + qi % g.nqx;
+        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx;
+        const size_t e = size_t(row) * a.topl + l;
+        const float* o = a.offsets + e * 3;
+        SampleDesc d;
+        d.kt = ti + int(roundf(__ldg(o)));
+        d.ok = d.kt >= 0 && d.kt < a.d.t;
+        if (!d.ok) {
+            latch(err_bit, err_code);
+            d.kt = ti;
+        }
+        const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+        const float fly = floorf(oy), flx = floorf(ox);
+        d.oy = int(fly);
+        d.ox = int(flx);
+        const float fy = oy - fly, fx = ox - flx;
+        const float wv = __ldg(a.weights + e);
+        d.w00 = wv * ((1.f - fy) * (1.f - fx));
+        d.w01 = wv * ((1.f - fy) * fx);
+        d.w10 = wv * (fy * (1.f - fx));
+        d.w11 = wv * (fy * fx);
+        desc[i] = d;
+    }
+}
+
+// Accumulate one unit (query at grid (gy, gx), sample at y + dy, x + dx where (dy, dx) is
+// the pixel's displacement inside the query's patch) for neighbours [l0, l1).
+template <int VEC>
+__device__ __forceinline__ void add_unit_tiled(const AggArgs& a, const SampleDesc* desc,
+                                               const TileGeom& g, int gy, int gx, int sy, int sx,
+                                               int l0, int l1, int c, float4& acc) {
+    const SampleDesc* dq = desc + ((gy - g.gy_lo) * g.nqx + (gx - g.gx_lo)) * a.topl;
+    const int H = a.d.h, W = a.d.w, F = a.d.f;
+    for (int l = l0; l < l1; ++l) {
+        const SampleDesc d = dq[l];
+        const int iy = sy + d.oy, ix = sx + d.ox;
+        const float* base = a.v + size_t(d.kt) * H * W * F + c;
+        const float *p00, *p01, *p10, *p11;
+        if (iy >= 0 && iy + 1 < H && ix >= 0 && ix + 1 < W) {
+            p00 = base + (size_t(iy) * W + ix) * F;
+            p01 = p00 + F;
+            p10 = p00 + size_t(W) * F;
+            p11 = p10 + F;
+        } else {  // reflected border taps (tensor.cpp:31-48)
+            const int y0 = reflect(iy, H), y1 = reflect(iy + 1, H);
+            const int x0 = reflect(ix, W), x1 = reflect(ix + 1, W);
+            p00 = base + (size_t(y0) * W + x0) * F;
+            p01 = base + (size_t(y0) * W + x1) * F;
+            p10 = base + (size_t(y1) * W + x0) * F;
+            p11 = base + (size_t(y1) * W + x1) * F;
+        }
+        const float4 A = __ldg(reinterpret_cast<const float4*>(p00));
+        const float4 B = __ldg(reinterpret_cast<const float4*>(p01));
+        const float4 C = __ldg(reinterpret_cast<const float4*>(p10));
+        const float4 D = __ldg(reinterpret_cast<const float4*>(p11));
+        acc.x = fmaf(d.w11, D.x, fmaf(d.w10, C.x, fmaf(d.w01, B.x, fmaf(d.w00, A.x, acc.x))));
+        acc.y = fmaf(d.w11, D.y, fmaf(d.w10, C.y, fmaf(d.w01, B.y, fmaf(d.w00, A.y, acc.y))));
+        acc.z = fmaf(d.w11, D.z, fmaf(d.w10, C.z, fmaf(d.w01, B.z, fmaf(d.w00, A.z, acc.z))));
+        acc.w = fmaf(d.w11, D.w, fmaf(d.w10, C.w, fmaf(d.w01, B.w, fmaf(d.w00, A.w, acc.w))));
+    }
+}
+
+// One pixel's fixed-order gather over neighbours [l0, l1) (aggregate.cpp:156-188).
+template <int VEC>
+__device__ int gather_tiled(const AggArgs& a, const SampleDesc* desc, const TileGeom& g, int y,
+                            int x, int l0, int l1, int c, float4& acc) {
+    const int st = a.d.stride0, half = a.ps / 2;
+    const int qmax_y = (a.d.nh - 1) * st, qmax_x = (a.d.nw - 1) * st;
+    int cnt = 0;
+    for (int py = -half; py <= half; ++py) {
+        const int qy = y - py;
+        if (qy < 0 || qy > qmax_y || qy % st != 0) continue;
+        for (int px = -half; px <= half; ++px) {
+            const int qx = x - px;
+            if (qx < 0 || qx > qmax_x || qx % st != 0) continue;
+            // footprint unit: sample at qy + off + py = y + off
+            add_unit_tiled<VEC>(a, desc, g, qy / st, qx / st, y, x, l0, l1, c, acc);
+            ++cnt;
+        }
+    }
+    const int qy = owner_index(y, st, a.d.nh) * st;
+    const int qx = owner_index(x, st, a.d.nw) * st;
+    if (abs(y - qy) > half || abs(x - qx) > half) {
+        add_unit_tiled<VEC>(a, desc, g, qy / st, qx / st, qy + clampi(y - qy, half),
+                            qx + clampi(x - qx, half), l0, l1, c, acc);
+        ++cnt;
+    }
+    return cnt;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __restrict__ out,
+                                                          int32_t* __restrict__ counts,
+                                                          int stack) {
+    extern __shared__ SampleDesc s_desc[];
+    constexpr int PPC = 256 / G;
+    const int tiles_x = (a.d.w + PPC - 1) / PPC;
+    const int tx = blockIdx.x % tiles_x;
+    const int y = (blockIdx.x / tiles_x) % a.d.h;
+    const int ti = blockIdx.x / (tiles_x * a.d.h);
+    const int x0 = tx * PPC;
+    const TileGeom g = tile_geom(a, y, x0, PPC);
+    build_descs(a, ti, g, s_desc, a.err, stack ? kErrStack : kErrWpsum);
+    __syncthreads();
+    const int p = threadIdx.x / G, c = (threadIdx.x % G) * 4;
+    const int x = x0 + p;
+    if (x >= a.d.w) return;
+    const size_t pix = (size_t(ti) * a.d.h + y) * a.d.w + x;
+    if (!stack) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int cnt = gather_tiled<4>(a, s_desc, g, y, x, 0, a.topl, c, acc);
+        if (cnt <= 0) {
+            latch(a.err, kErrWpsum);
+            return;
+        }
+        if (c == 0 && counts) counts[pix] = cnt;
+        const float fc = float(cnt);
+        *reinterpret_cast<float4*>(out + pix * a.d.f + c) =
+            make_float4(acc.x / fc, acc.y / fc, acc.z / fc, acc.w / fc);
+    } else {
+        const size_t plane = size_t(a.d.t) * a.d.h * a.d.w * a.d.f;
+        for (int l = 0; l < a.topl; ++l) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            gather_tiled<4>(a, s_desc, g, y, x, l, l + 1, c, acc);
+            *reinterpret_cast<float4*>(out + l * plane + pix * a.d.f + c) = acc;
+        }
+    }
+}
+
+template <int G>
+int launch_tiled_agg(const AggArgs& a, float* out, int32_t* counts, int stack, cudaStream_t st) {
+    constexpr int PPC = 256 / G;
+    const int s0 = a.d.stride0;
+    const int nqy = 3 + 1, nqx = (PPC + 2 * s0) / s0 + 3;
+    const size_t smem = size_t(nqy) * nqx * a.topl * sizeof(SampleDesc);
+    if (smem > 200 * 1024) return 0;
+    cudaFuncSetAttribute(wpsum_tiled_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const int tiles_x = (a.d.w + PPC - 1) / PPC;
+    const unsigned blocks = unsigned(int64_t(a.d.t) * a.d.h * tiles_x);
+    wpsum_tiled_kernel<G><<<blocks, 256, smem, st>>>(a, out, counts, stack);
+    return 1;
+}
+
+int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stack, cudaStream_t st) {
+    if (a.d.f % 4 != 0) return 0;
+    switch (a.d.f / 4) {
+        case 1: return launch_tiled_agg<1>(a, out, counts, stack, st);
+        case 2: return launch_tiled_agg<2>(a, out, counts, stack, st);
+        case 4: return launch_tiled_agg<4>(a, out, counts, stack, st);
+        case 8: return launch_tiled_agg<8>(a, out, counts, stack, st);
+        case 16: return launch_tiled_agg<16>(a, out, counts, stack, st);
+        case 32: return launch_tiled_agg<32>(a, out, counts, stack, st);
+        default: return 0;
+    }
+}
+
 // softmax_rows (aggregate.cpp:16-37): one thread per row.
 __global__ void softmax_kernel(int64_t rows, int l, float beta, const float* __restrict__ sims,
                                float* __restrict__ w, int* err) {
@@ -248,6 +442,7 @@ int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* we
 }
 
 int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
+    if (int n = launch_tiled_agg_any(a, out, counts, 0, st)) return n;
     const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {
         const int64_t n = npix * (a.d.f / 4);
@@ -260,6 +455,7 @@ int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st)
 }
 
 int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st) {
+    if (int n = launch_tiled_agg_any(a, out, nullptr, 1, st)) return n;
     const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {
         const int64_t n = npix * (a.d.f / 4) * a.topl;

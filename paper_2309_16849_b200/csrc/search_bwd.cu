@@ -48,36 +48,41 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
             const size_t iq = vidx(d, qt, ry, rx) + c;
             const size_t i00 = vidx(d, kt, t.y0, t.x0) + c, i01 = vidx(d, kt, t.y0, t.x1) + c;
             const size_t i10 = vidx(d, kt, t.y1, t.x0) + c, i11 = vidx(d, kt, t.y1, t.x1) + c;
-            float sy = 0.f, sx = 0.f;
+            // dS/d(ky, kx) sums hundreds of cancelling terms per entry: keep that chain in
+            // fp64 (the dQ/dK scatter stays fp32)
+            const double dfy = fy, dfx = fx;
+            const double w00 = (1.0 - dfy) * (1.0 - dfx), w01 = (1.0 - dfy) * dfx;
+            const double w10 = dfy * (1.0 - dfx), w11 = dfy * dfx;
+            double sy = 0.0, sx = 0.0;
 #pragma unroll
             for (int j = 0; j < VEC; ++j) {
                 const float qv = __ldg(q + iq + j);
                 const float k00 = __ldg(k + i00 + j), k01 = __ldg(k + i01 + j);
                 const float k10 = __ldg(k + i10 + j), k11 = __ldg(k + i11 + j);
-                const float kv = blend(t, k00, k01, k10, k11);
-                float ds_dq, ds_dk;
+                const double kv = w00 * k00 + w01 * k01 + w10 * k10 + w11 * k11;
+                double ds_dq, ds_dk;
                 if (metric == SNLS_METRIC_IP) {
                     ds_dq = kv;
                     ds_dk = qv;
                 } else {
-                    const float diff = qv - kv;
-                    ds_dq = -2.f * diff;
-                    ds_dk = 2.f * diff;
+                    const double diff = double(qv) - kv;
+                    ds_dq = -2.0 * diff;
+                    ds_dk = 2.0 * diff;
                 }
-                const float gq = g * ds_dq, gk = g * ds_dk;
-                atomicAdd(dq + iq + j, gq);
-                atomicAdd(dk + i00 + j, gk * t.w00);
-                atomicAdd(dk + i01 + j, gk * t.w01);
-                atomicAdd(dk + i10 + j, gk * t.w10);
-                atomicAdd(dk + i11 + j, gk * t.w11);
+                const double gk = double(g) * ds_dk;
+                atomicAdd(dq + iq + j, float(double(g) * ds_dq));
+                atomicAdd(dk + i00 + j, float(gk * w00));
+                atomicAdd(dk + i01 + j, float(gk * w01));
+                atomicAdd(dk + i10 + j, float(gk * w10));
+                atomicAdd(dk + i11 + j, float(gk * w11));
                 // d(sample)/dy, d(sample)/dx from the tap values (search.cpp:574-577)
-                const float dkv_dy = (1.f - fx) * (k10 - k00) + fx * (k11 - k01);
-                const float dkv_dx = (1.f - fy) * (k01 - k00) + fy * (k11 - k10);
-                sy = fmaf(gk, dkv_dy, sy);
-                sx = fmaf(gk, dkv_dx, sx);
+                const double dkv_dy = (1.0 - dfx) * (double(k10) - k00) + dfx * (double(k11) - k01);
+                const double dkv_dx = (1.0 - dfy) * (double(k01) - k00) + dfy * (double(k11) - k10);
+                sy += gk * dkv_dy;
+                sx += gk * dkv_dx;
             }
-            gy += double(sy);
-            gx += double(sx);
+            gy += sy;
+            gx += sx;
         }
     }
     atomicAdd(gyx + 2 * e, gy);

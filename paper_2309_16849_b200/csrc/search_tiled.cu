@@ -77,23 +77,32 @@ __device__ __forceinline__ float accum4(float acc, const float4& q, const float4
     return acc;
 }
 
-// Register top-L list, sorted descending; candidates arrive in ascending slot order.
-template <int KMAX>
-__device__ __forceinline__ void topl_push(float (&tv)[KMAX], uint32_t (&ts)[KMAX], float v,
-                                          uint32_t s) {
-    if (!(v > tv[KMAX - 1])) return;
+// Group-wide top-L list, rank-sharded over the G lanes of a query: lane gl holds ranks
+// [gl*M, gl*M+M) of one list sorted descending (M = KMAX/G).  Candidates reach it in
+// ascending slot order and are inserted with strict '>' -- the reference's topl_insert
+// (search.cpp:187-197) -- so equal values never displace an earlier slot.  The list's last
+// rank is the exact group threshold, so almost every candidate is rejected by one compare.
+template <int G, int M>
+__device__ __forceinline__ void group_insert(float (&ev)[M], uint32_t (&es)[M], float v,
+                                             uint32_t s, int gl) {
+    // the entry just above mine is the previous lane's last one (+inf above rank 0)
+    float pv = __shfl_up_sync(0xffffffffu, ev[M - 1], 1, G);
+    uint32_t ps = __shfl_up_sync(0xffffffffu, es[M - 1], 1, G);
+    if (gl == 0) pv = INFINITY;
+    float nv[M];
+    uint32_t ns[M];
 #pragma unroll
-    for (int j = KMAX - 1; j > 0; --j) {
-        const bool gp = v > tv[j - 1];
-        const bool gc = v > tv[j];
-        const float nv = gp ? tv[j - 1] : (gc ? v : tv[j]);
-        const uint32_t ns = gp ? ts[j - 1] : (gc ? s : ts[j]);
-        tv[j] = nv;
-        ts[j] = ns;
+    for (int j = 0; j < M; ++j) {
+        const float above = j == 0 ? pv : ev[j - 1];
+        const uint32_t above_s = j == 0 ? ps : es[j - 1];
+        const bool ga = v > above, gc = v > ev[j];
+        nv[j] = ga ? above : (gc ? v : ev[j]);
+        ns[j] = ga ? above_s : (gc ? s : es[j]);
     }
-    if (v > tv[0]) {
-        tv[0] = v;
-        ts[0] = s;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        ev[j] = nv[j];
+        es[j] = ns[j];
     }
 }
 
@@ -126,13 +135,15 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
         qcol[p] = reflect_near(qx + p - HP, Wd) * F;
     }
 
-    float tv[KMAX];
-    uint32_t ts[KMAX];
+    constexpr int M = KMAX / G;  // ranks per lane
+    float ev[M];
+    uint32_t es[M];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        tv[j] = -INFINITY;
-        ts[j] = 0xffffffffu;
+    for (int j = 0; j < M; ++j) {
+        ev[j] = -INFINITY;
+        es[j] = 0xffffffffu;
     }
+    const int glast = (lane / G) * G + (G - 1);  // lane holding the group's last rank
 
     for (int fp = 0; fp < nfr; ++fp) {
         const int dt = scan_dt(fp), kt = qt + dt;
@@ -203,41 +214,47 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
                     }
                 }
                 const int arow = r - (P - 1);
+                // exact group threshold = current last rank; most candidates stop here
+                const float thr = __shfl_sync(0xffffffffu, ev[M - 1], glast);
+                uint32_t pend = 0;
 #pragma unroll
                 for (int i = 0; i < C::NPL; ++i) {
                     const int b = gl * C::NPL + i;
-                    const float val = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
-                    if (on && b < W) topl_push<KMAX>(tv, ts, val, slot_base + uint32_t(arow * W + b));
+                    v[i] = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
+                    if (on && b < W && v[i] > thr) pend |= 1u << i;
                 }
+                // insert the survivors one at a time, lanes then slots ascending (= slot order)
+                while (__any_sync(0xffffffffu, pend != 0)) {
+                    const unsigned want = __ballot_sync(0xffffffffu, pend != 0);
+                    const unsigned gmask = (want >> (gq * G)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
+                    const int src = gmask ? gq * G + (__ffs(gmask) - 1) : lane;
+                    const int isrc = pend ? (__ffs(pend) - 1) : 0;
+                    float cv = -INFINITY;
 #pragma unroll
-                for (int s = 0; s + 1 < P; ++s)
-#pragma unroll
-                    for (int b = 0; b < W; ++b) acc[s][b] = acc[s + 1][b];
-#pragma unroll
-                for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
+                    for (int i = 0; i < C::NPL; ++i) cv = (i == isrc) ? v[i] : cv;
+                    const uint32_t cs = slot_base + uint32_t(arow * W + gl * C::NPL + isrc);
+                    float bv = __shfl_sync(0xffffffffu, cv, src);
+                    const uint32_t bs = __shfl_sync(0xffffffffu, cs, src);
+                    if (!gmask) bv = -INFINITY;  // no-op insert keeps the shuffles warp-uniform
+                    group_insert<G, M>(ev, es, bv, bs, gl);
+                    if (lane == src && gmask) pend &= pend - 1;
+                }
             }
+            // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one
+#pragma unroll
+            for (int s = 0; s + 1 < P; ++s)
+#pragma unroll
+                for (int b = 0; b < W; ++b) acc[s][b] = acc[s + 1][b];
+#pragma unroll
+            for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
         }
     }
 
-    // ---- merge the G lane lists: topl rounds of a (value desc, slot asc) max -------------
-    for (int li = 0; li < a.topl; ++li) {
-        const uint64_t mine = eligible(tv[0]) ? pack_key(tv[0], ts[0]) : 0ull;
-        uint64_t best = mine;
+    // ---- the group list is already the merged top-KMAX: lane gl owns ranks gl*M .. gl*M+M-1
 #pragma unroll
-        for (int m = G / 2; m >= 1; m >>= 1) {
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, best, m);
-            best = o > best ? o : best;
-        }
-        if (gl == 0) s_keys[qslot][li] = best;
-        if (best != 0ull && mine == best) {
-#pragma unroll
-            for (int j = 0; j + 1 < KMAX; ++j) {
-                tv[j] = tv[j + 1];
-                ts[j] = ts[j + 1];
-            }
-            tv[KMAX - 1] = -INFINITY;
-            ts[KMAX - 1] = 0xffffffffu;
-        }
+    for (int j = 0; j < M; ++j) {
+        const int li = gl * M + j;
+        if (li < a.topl) s_keys[qslot][li] = eligible(ev[j]) ? pack_key(ev[j], es[j]) : 0ull;
     }
     __syncwarp();
 

@@ -28,12 +28,48 @@ def gpu_bwd(q, k, cfg, offsets, chains_abs, grad):
     return [host(x) for x in S.shifted_nls_backward(dev(grad), res, dev(q), dev(k))]
 
 
+def centers_from(offsets32, cfg, t, h, w):
+    """The reference tape (absolute fp64 centres) that the fp32 device tape encodes."""
+    rows = offsets32.shape[0]
+    nh, nw = (h - 1) // cfg.stride0 + 1, (w - 1) // cfg.stride0 + 1
+    r = np.arange(rows)
+    base = np.stack([r // (nh * nw), ((r // nw) % nh) * cfg.stride0, (r % nw) * cfg.stride0], -1)
+    return base[:, None, :].astype(np.float64) + offsets32.astype(np.float32).astype(np.float64)
+
+
+def abs_chains(chains_abs64, cfg, t, h, w, offsets):
+    """fp64 reference chains -> fp32 relative device chains -> back to absolute fp64."""
+    rel = rel_chains(chains_abs64, cfg, t, h, w, offsets).astype(np.float32).astype(np.float64)
+    return rel_chains_inverse(rel, chains_abs64, cfg, t, h, w, offsets)
+
+
+def rel_chains_inverse(rel, chains_abs64, cfg, t, h, w, offsets):
+    out = rel.copy()
+    if out.size == 0:
+        return out
+    back = rel_chains(np.zeros_like(chains_abs64), cfg, t, h, w, offsets)  # = -q on used links
+    out[..., 0] -= back[..., 0]
+    out[..., 1] -= back[..., 1]
+    return out
+
+
 @pytest.mark.parametrize("name", ["c2_mini", "c4_mini", "stride_half", "zero_flow"])
-def test_golden_backward(name):
+def test_golden_backward(name, port):
+    """Stage-isolated on the reference's own tape.  The device tape is fp32 (offsets, relative
+    chain links); identical inputs for the backward therefore means the same fp32 tape on
+    both sides, and every gradient must then agree to REL_TOL.  Against the reference's fp64
+    tape the flow gradients additionally carry the tape rounding (d(dS/dy)/dy ~ 2*sum(dk/dy)^2
+    times ~2e-7 px): that distance is bounded separately at 1e-4."""
     z, cfg = load(name)
+    t, h, w, _ = z["q"].shape
     dq, dk, dff, dbf = gpu_bwd(z["q"], z["k"], cfg, z["offsets"], z["chains"], z["grad_sims"])
+    same = port.search_bwd(z["q"], z["k"], cfg, centers_from(z["offsets"], cfg, t, h, w),
+                           abs_chains(z["chains"], cfg, t, h, w, z["offsets"]),
+                           z["grad_sims"].astype(np.float64))
     for got, key in ((dq, "dq"), (dk, "dk"), (dff, "dfflow"), (dbf, "dbflow")):
-        assert max_rel(got, z[key]) <= REL_TOL, (key, max_rel(got, z[key]))
+        assert max_rel(got, same[key]) <= REL_TOL, (key, max_rel(got, same[key]))
+        bound = REL_TOL if key in ("dq", "dk") else 1e-4
+        assert max_rel(got, z[key]) <= bound, (key, max_rel(got, z[key]))
 
 
 def test_random_backward_vs_oracle(port):

@@ -250,29 +250,52 @@ __device__ __forceinline__ void add_unit_tiled(const AggArgs& a, const SampleDes
     }
 }
 
-// One pixel's fixed-order gather over neighbours [l0, l1) (aggregate.cpp:156-188).
+// Footprint units along one axis: the patch offsets p in [-half, half] with coord - p on the
+// query grid {0, s0, ..., qmax}.  Since half < s0 there are at most two, p = m and p = m - s0
+// with m = coord mod s0 (ascending p order, as the reference loops, aggregate.cpp:161-166).
+struct AxisUnits {
+    int n, p0, p1;
+};
+__device__ __forceinline__ AxisUnits axis_units(int coord, int s0, int half, int qmax) {
+    const int m = coord % s0;
+    AxisUnits u;
+    u.n = 0;
+    u.p0 = u.p1 = 0;
+    const int cand[2] = {m - s0, m};  // ascending
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int p = cand[i], q = coord - p;
+        if (p >= -half && p <= half && q >= 0 && q <= qmax) {
+            if (u.n == 0) u.p0 = p; else u.p1 = p;
+            ++u.n;
+        }
+    }
+    return u;
+}
+
+// One pixel's fixed-order gather over neighbours [l0, l1) (aggregate.cpp:156-188), with the
+// footprint units enumerated without division in the inner loop.
 template <int VEC>
-__device__ int gather_tiled(const AggArgs& a, const SampleDesc* desc, const TileGeom& g, int y,
-                            int x, int l0, int l1, int c, float4& acc) {
+__device__ int gather_tiled(const AggArgs& a, const SampleDesc* desc, const TileGeom& g,
+                            const AxisUnits& uy, int y, int x, int l0, int l1, int c,
+                            float4& acc) {
     const int st = a.d.stride0, half = a.ps / 2;
-    const int qmax_y = (a.d.nh - 1) * st, qmax_x = (a.d.nw - 1) * st;
+    const AxisUnits ux = axis_units(x, st, half, (a.d.nw - 1) * st);
     int cnt = 0;
-    for (int py = -half; py <= half; ++py) {
-        const int qy = y - py;
-        if (qy < 0 || qy > qmax_y || qy % st != 0) continue;
-        for (int px = -half; px <= half; ++px) {
-            const int qx = x - px;
-            if (qx < 0 || qx > qmax_x || qx % st != 0) continue;
+    for (int iy = 0; iy < uy.n; ++iy) {
+        const int py = iy == 0 ? uy.p0 : uy.p1;
+        for (int ix = 0; ix < ux.n; ++ix) {
+            const int px = ix == 0 ? ux.p0 : ux.p1;
             // footprint unit: sample at qy + off + py = y + off
-            add_unit_tiled<VEC>(a, desc, g, qy / st, qx / st, y, x, l0, l1, c, acc);
+            add_unit_tiled<VEC>(a, desc, g, (y - py) / st, (x - px) / st, y, x, l0, l1, c, acc);
             ++cnt;
         }
     }
-    const int qy = owner_index(y, st, a.d.nh) * st;
-    const int qx = owner_index(x, st, a.d.nw) * st;
+    const int gy = owner_index(y, st, a.d.nh), gx = owner_index(x, st, a.d.nw);
+    const int qy = gy * st, qx = gx * st;
     if (abs(y - qy) > half || abs(x - qx) > half) {
-        add_unit_tiled<VEC>(a, desc, g, qy / st, qx / st, qy + clampi(y - qy, half),
-                            qx + clampi(x - qx, half), l0, l1, c, acc);
+        add_unit_tiled<VEC>(a, desc, g, gy, gx, qy + clampi(y - qy, half), qx + clampi(x - qx, half),
+                            l0, l1, c, acc);
         ++cnt;
     }
     return cnt;
@@ -295,10 +318,11 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
     const int p = threadIdx.x / G, c = (threadIdx.x % G) * 4;
     const int x = x0 + p;
     if (x >= a.d.w) return;
+    const AxisUnits uy = axis_units(y, a.d.stride0, a.ps / 2, (a.d.nh - 1) * a.d.stride0);
     const size_t pix = (size_t(ti) * a.d.h + y) * a.d.w + x;
     if (!stack) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int cnt = gather_tiled<4>(a, s_desc, g, y, x, 0, a.topl, c, acc);
+        const int cnt = gather_tiled<4>(a, s_desc, g, uy, y, x, 0, a.topl, c, acc);
         if (cnt <= 0) {
             latch(a.err, kErrWpsum);
             return;
@@ -311,7 +335,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
         const size_t plane = size_t(a.d.t) * a.d.h * a.d.w * a.d.f;
         for (int l = 0; l < a.topl; ++l) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            gather_tiled<4>(a, s_desc, g, y, x, l, l + 1, c, acc);
+            gather_tiled<4>(a, s_desc, g, uy, y, x, l, l + 1, c, acc);
             *reinterpret_cast<float4*>(out + l * plane + pix * a.d.f + c) = acc;
         }
     }

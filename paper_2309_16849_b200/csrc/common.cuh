@@ -51,10 +51,15 @@ __device__ __forceinline__ int reflect(int i, int n) {
     return m < n ? m : period - m;
 }
 
-// Cheap reflect for |overshoot| < n (the common case near borders).
+static __device__ __noinline__ int reflect_far(int i, int n) { return reflect(i, n); }
+
+// Reflect with the single-fold cases inline (two compares, no division): -i and
+// 2(n-1)-i are symmetries of the period-2(n-1) mirror, so applying them first and the full
+// reflect only to what is still out of range gives reflect(i, n) exactly.
 __device__ __forceinline__ int reflect_near(int i, int n) {
-    if (i >= 0 && i < n) return i;
-    return reflect(i, n);
+    i = i < 0 ? -i : i;
+    i = i >= n ? 2 * (n - 1) - i : i;
+    return unsigned(i) < unsigned(n) ? i : reflect_far(i, n);
 }
 
 // search.cpp:52-57

@@ -157,10 +157,15 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
         const int by = int(fby) - HW - HP, bx = int(fbx) - HW - HP;
-        const float* kbase = a.k + size_t(on ? kt : qt) * frame_elems + c0;
-        int xo[R + 1];
+        // float4-granular addressing: per region row one 64-bit row base, per column a
+        // 32-bit float4 index (one IMAD.WIDE per load instead of 64-bit pointer math)
+        const float4* kbase = reinterpret_cast<const float4*>(a.k + size_t(on ? kt : qt) * frame_elems) + gl;
+        const unsigned row4 = unsigned(Wd) * G;  // float4 per image row
+        unsigned xo[R + 1];
 #pragma unroll
-        for (int j = 0; j <= R; ++j) xo[j] = reflect_near(bx + j, Wd) * F;
+        for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * G;
+        const bool interior = __all_sync(0xffffffffu, bx >= 0 && bx + R < Wd);
+        const unsigned xb = unsigned(bx) * G;
 
         float acc[P][W];
 #pragma unroll
@@ -172,14 +177,28 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
-            const float* r0 = kbase + size_t(reflect_near(by + r, H)) * Wd * F;
-            const float* r1 = kbase + size_t(reflect_near(by + r + 1, H)) * Wd * F;
+            const unsigned r0 = unsigned(reflect_near(by + r, H)) * row4;
+            const unsigned r1 = unsigned(reflect_near(by + r + 1, H)) * row4;
             float4 kr[R];
-            {
-                float4 a0 = V::ld(r0 + xo[0]), a1 = V::ld(r1 + xo[0]);
+            if (interior) {
+                // no column reflection anywhere in the warp: one 64-bit base per raw row and
+                // compile-time offsets (LDG [R + imm]) for the ws+ps columns
+                const float4* p0 = kbase + (r0 + xb);
+                const float4* p1 = kbase + (r1 + xb);
+                float4 a0 = __ldg(p0), a1 = __ldg(p1);
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    const float4 b0 = V::ld(r0 + xo[j + 1]), b1 = V::ld(r1 + xo[j + 1]);
+                    const float4 b0 = __ldg(p0 + (j + 1) * G), b1 = __ldg(p1 + (j + 1) * G);
+                    kr[j] = lerp4(a0, b0, a1, b1, w00, w01, w10, w11);
+                    a0 = b0;
+                    a1 = b1;
+                }
+            } else {
+                float4 a0 = __ldg(kbase + (r0 + xo[0])), a1 = __ldg(kbase + (r1 + xo[0]));
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const float4 b0 = __ldg(kbase + (r0 + xo[j + 1]));
+                    const float4 b1 = __ldg(kbase + (r1 + xo[j + 1]));
                     kr[j] = lerp4(a0, b0, a1, b1, w00, w01, w10, w11);
                     a0 = b0;
                     a1 = b1;

@@ -90,6 +90,13 @@ int snls_ctx_last_search_path(snls_ctx* ctx, int* out);
 /* Force the generic per-slot search path (1) or allow the tiled one (0, default). */
 int snls_ctx_force_generic(snls_ctx* ctx, int on);
 
+/* ---- device memory through the context (so C++ callers need no CUDA headers) --------- */
+int snls_device_alloc(snls_ctx* ctx, uint64_t bytes, void** out);
+int snls_device_free(snls_ctx* ctx, void* ptr);
+/* Stream-ordered copies; snls_copy_d2h returns after the data has landed. */
+int snls_copy_h2d(snls_ctx* ctx, void* dst_device, const void* src_host, uint64_t bytes);
+int snls_copy_d2h(snls_ctx* ctx, void* dst_host, const void* src_device, uint64_t bytes);
+
 /* ---- search (search.hpp) ------------------------------------------------------------ */
 /* Replaces snls::shifted_nls_forward (search.hpp:126-128; search.cpp:414-421).
  * fflow/bflow may be NULL for zero flows (snls::nls_forward, search.hpp:131-132).

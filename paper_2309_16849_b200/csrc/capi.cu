@@ -247,6 +247,48 @@ int snls_ctx_sync_check(snls_ctx* ctx) {
     return fail(SNLS_EDOMAIN, "snls: device reported an unknown domain error");
 }
 
+int snls_device_alloc(snls_ctx* ctx, uint64_t bytes, void** out) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (!out) return fail(SNLS_EARG, "snls_device_alloc: null output");
+    DeviceGuard g(ctx->device);
+    *out = nullptr;
+    if (bytes == 0) return SNLS_OK;
+    const cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_device_alloc");
+    return SNLS_OK;
+}
+
+int snls_device_free(snls_ctx* ctx, void* ptr) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (!ptr) return SNLS_OK;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    const cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_device_free");
+    return SNLS_OK;
+}
+
+int snls_copy_h2d(snls_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (bytes == 0) return SNLS_OK;
+    if (!dst || !src) return fail(SNLS_EARG, "snls_copy_h2d: null pointer");
+    DeviceGuard g(ctx->device);
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_copy_h2d");
+    return SNLS_OK;
+}
+
+int snls_copy_d2h(snls_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (bytes == 0) return SNLS_OK;
+    if (!dst || !src) return fail(SNLS_EARG, "snls_copy_d2h: null pointer");
+    DeviceGuard g(ctx->device);
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_copy_d2h");
+    return SNLS_OK;
+}
+
 static int search_common_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                                 const float* q, const float* k, const float* ff, const float* bf) {
     if (int rc = check_ctx(ctx)) return rc;

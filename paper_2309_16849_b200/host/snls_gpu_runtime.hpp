@@ -1,0 +1,51 @@
+// Host runtime of the drop-in adapter: a per-thread device context, grow-only device
+// buffers, fp64 <-> fp32 staging, and the status -> exception mapping of the reference
+// (errors.hpp:9-17).  Everything device-side goes through the C-ABI in include/snls_cuda.h.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "snls/errors.hpp"
+#include "snls/search.hpp"
+#include "snls_cuda.h"
+
+namespace snls::gpu {
+
+// Throws the reference's exception type for a C-ABI status (same message text).
+void check(int status);
+
+// Context for the calling thread: device from $SNLS_DEVICE (default 0), default stream.
+snls_ctx* context();
+
+// A device allocation that only grows; one per role so repeated calls reuse memory.
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    ~DeviceBuffer();
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+
+    void* reserve(std::uint64_t bytes);
+    float* f32(std::uint64_t n) { return static_cast<float*>(reserve(n * sizeof(float))); }
+    std::int32_t* i32(std::uint64_t n) {
+        return static_cast<std::int32_t*>(reserve(n * sizeof(std::int32_t)));
+    }
+
+private:
+    void* ptr_ = nullptr;
+    std::uint64_t bytes_ = 0;
+};
+
+// fp64 host data -> fp32 device buffer (the reference computes in fp64, the kernels in
+// fp32; fp32-representable inputs round-trip exactly).
+float* upload(DeviceBuffer& buf, const std::vector<double>& host);
+float* upload(DeviceBuffer& buf, const double* host, std::uint64_t n);
+std::int32_t* upload_i32(DeviceBuffer& buf, const std::vector<std::int32_t>& host);
+void download(std::vector<double>& host, const float* dev, std::uint64_t n);
+void download_i32(std::vector<std::int32_t>& host, const std::int32_t* dev, std::uint64_t n);
+
+snls_config to_abi(const snls::SearchConfig& cfg);
+
+}  // namespace snls::gpu

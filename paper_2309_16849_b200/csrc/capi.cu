@@ -314,30 +314,40 @@ int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const
     const float beta = float(cfg->softmax_scale);
 
     if (mode == SNLS_MODE_FULLGRID) {
+        // materialise rows x window_slots scores (search.cpp:351-376) with the same kernel
+        // arithmetic as the fused path, then select + emit from the grid (search.cpp:378-406):
+        // fused and full-grid results are bitwise identical, as in the reference.
         const int n = (2 * cfg->wt + 1) * cfg->ws * cfg->ws;
-        const size_t need = size_t(d.rows) * n * 4 * sizeof(float);
-        if (int rc = ensure_work(ctx, need)) return rc;
+        if (int rc = ensure_work(ctx, size_t(d.rows) * n * sizeof(float))) return rc;
         float* grid = static_cast<float*>(ctx->work);
-        float* goff = grid + size_t(d.rows) * n;
-        GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
-                         cfg->stride1, beta, sims, offsets, nullptr, nullptr, grid, goff, 0, ctx->err};
-        if (launch_search_generic(gs, ctx->stream) < 0)
-            return fail(SNLS_ECONFIG, "search: window too large for the device search");
-        ++launched;
-        if (launch_topl(d.rows, n, grid, goff, cfg->topl, sims, offsets, ctx->err, ctx->stream) < 0)
+        int produced = 0;
+        if (!ctx->force_generic && cfg->stride1 == 1.0) {
+            TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
+                           sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid};
+            produced = launch_search_tiled(ts, ctx->stream);
+            if (produced < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
+        }
+        if (produced == 0) {
+            GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
+                             cfg->stride1, beta, sims, offsets, nullptr, nullptr, grid, nullptr, 0,
+                             ctx->err, nullptr};
+            if (launch_search_generic(gs, ctx->stream) < 0)
+                return fail(SNLS_ECONFIG, "search: window too large for the device search");
+            produced = 1;
+        }
+        GenericSearch sel{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
+                          cfg->stride1, beta, sims, offsets, chains, weights, nullptr, nullptr, 1,
+                          ctx->err, grid};
+        if (launch_search_generic(sel, ctx->stream) < 0)
             return fail(SNLS_ECONFIG, "search: window too large for the device top_l");
-        ++launched;
-        if (chains && cfg->wt > 1)
-            launched += launch_emit_tape(ff, bf, d, cfg->wt, cfg->topl, offsets, chains, ctx->stream);
-        if (weights) launched += launch_softmax(d.rows, cfg->topl, beta, sims, weights, ctx->err, ctx->stream);
-        ctx->last_path = 0;
-        return after_launch(ctx, launched, "snls_search_fwd(fullgrid)");
+        ctx->last_path = 2;
+        return after_launch(ctx, launched + produced + 1, "snls_search_fwd(fullgrid)");
     }
 
     int tiled = 0;
     if (!ctx->force_generic && cfg->stride1 == 1.0) {
         TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
-                       sims, offsets, chains, weights, ctx->err, ctx->num_sms};
+                       sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr};
         tiled = launch_search_tiled(ts, ctx->stream);
         if (tiled < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
     }
@@ -346,7 +356,8 @@ int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const
         ctx->last_path = 1;
     } else {
         GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
-                         cfg->stride1, beta, sims, offsets, chains, weights, nullptr, nullptr, 1, ctx->err};
+                         cfg->stride1, beta, sims, offsets, chains, weights, nullptr, nullptr, 1, ctx->err,
+                         nullptr};
         if (launch_search_generic(gs, ctx->stream) < 0)
             return fail(SNLS_ECONFIG, "search: window too large for the device search");
         ++launched;
@@ -364,7 +375,8 @@ int snls_search_grid(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, cons
     const Dims d = make_dims(dims, cfg->stride0);
     int launched = launch_flows_check(ff, bf, int64_t(dims.t) * dims.h * dims.w * 2, ctx->err, ctx->stream);
     GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
-                     cfg->stride1, 1.f, nullptr, nullptr, nullptr, nullptr, grid, grid_offsets, 0, ctx->err};
+                     cfg->stride1, 1.f, nullptr, nullptr, nullptr, nullptr, grid, grid_offsets, 0, ctx->err,
+                     nullptr};
     if (launch_search_generic(gs, ctx->stream) < 0)
         return fail(SNLS_ECONFIG, "search: window too large for the device search");
     return after_launch(ctx, launched + 1, "snls_search_grid");

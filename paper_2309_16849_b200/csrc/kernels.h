@@ -20,6 +20,7 @@ struct GenericSearch {
     float *grid, *grid_offsets;
     int select;
     int* err;
+    const float* grid_in;  // select from an already materialised grid instead of computing
 };
 
 struct TiledSearch {
@@ -30,6 +31,7 @@ struct TiledSearch {
     float *sims, *offsets, *chains, *weights;
     int* err;
     int num_sms;
+    float* grid;  // kFullGrid: write every window score (rows x slots) and skip selection
 };
 
 struct AggArgs {

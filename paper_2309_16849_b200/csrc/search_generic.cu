@@ -114,6 +114,7 @@ struct SearchArgs {
     float* grid_offsets;  // optional rows x n x 3
     int select;           // 0: only write the grid
     int* err;
+    const float* grid_in;  // candidates already materialised (full-grid mode)
 };
 
 template <int VEC>
@@ -143,7 +144,8 @@ __global__ void __launch_bounds__(128) search_generic_kernel(SearchArgs a) {
     }
     __syncwarp();
 
-    for (int s = lane; s < n; s += 32) {
+    for (int s = lane; a.grid_in && s < n; s += 32) cand[s] = a.grid_in[size_t(row) * n + s];
+    for (int s = lane; !a.grid_in && s < n; s += 32) {
         const int fp = s / ss, rem = s % ss;
         const int dt = scan_dt(fp), kt = qt + dt;
         const int dyi = rem / a.ws, dxi = rem % a.ws;
@@ -339,6 +341,7 @@ int launch_search_generic(const GenericSearch& g, cudaStream_t st) {
     a.grid_offsets = g.grid_offsets;
     a.select = g.select;
     a.err = g.err;
+    a.grid_in = g.grid_in;
     const size_t smem = per_warp * warps;
     const unsigned blocks = unsigned((g.d.rows + warps - 1) / warps);
     if (g.d.f % 4 == 0) {

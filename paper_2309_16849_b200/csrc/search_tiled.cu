@@ -106,6 +106,12 @@ __device__ __forceinline__ void group_insert(float (&ev)[M], uint32_t (&es)[M], 
     }
 }
 
+template <int W, int G>
+__device__ __forceinline__ void write_off_frame(float* grid, int64_t row, int fp, int nfr, int gl) {
+    float* g = grid + size_t(row) * nfr * W * W + size_t(fp) * W * W;
+    for (int s = gl; s < W * W; s += G) g[s] = -INFINITY;
+}
+
 template <int P, int W, int VEC, int G, int KMAX, int METRIC>
 __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G, KMAX>;
@@ -148,7 +154,10 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
     for (int fp = 0; fp < nfr; ++fp) {
         const int dt = scan_dt(fp), kt = qt + dt;
         const bool on = row_ok && kt >= 0 && kt < a.d.t;
-        if (!__any_sync(0xffffffffu, on)) continue;  // warp-uniform skip (search.cpp:300)
+        if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
+            if (a.grid && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
+            continue;
+        }
         double sdy = 0.0, sdx = 0.0;
         if (on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
         const double cy = double(qy) + sdy, cx = double(qx) + sdx;
@@ -233,6 +242,16 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
                     }
                 }
                 const int arow = r - (P - 1);
+                if (a.grid) {  // kFullGrid: materialise the scores (-inf off-clip), no selection
+#pragma unroll
+                    for (int i = 0; i < C::NPL; ++i) {
+                        const int b = gl * C::NPL + i;
+                        const float val = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
+                        if (row_ok && b < W)
+                            a.grid[size_t(row) * nfr * W * W + slot_base + arow * W + b] = on ? val : -INFINITY;
+                    }
+                    goto rotate;
+                }
                 // exact group threshold = current last rank; most candidates stop here
                 const float thr = __shfl_sync(0xffffffffu, ev[M - 1], glast);
                 uint32_t pend = 0;
@@ -259,6 +278,7 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
                     if (lane == src && gmask) pend &= pend - 1;
                 }
             }
+        rotate:
             // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)
@@ -268,6 +288,8 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
             for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
         }
     }
+
+    if (a.grid) return;  // selection happens in the top_l pass over the grid
 
     // ---- the group list is already the merged top-KMAX: lane gl owns ranks gl*M .. gl*M+M-1
 #pragma unroll

@@ -89,7 +89,7 @@ struct RefSearch {
 };
 
 static RefSearch ref_search(const VideoTensor& q, const VideoTensor& k, const FlowField& ff,
-                            const FlowField& bf, const SearchConfig& cfg) {
+                            const FlowField& bf, const SearchConfig& cfg, bool quiet = false) {
     const QueryGrid g = QueryGrid::over(q.t, q.h, q.w, cfg.stride0);
     const std::size_t n = std::size_t(g.rows()) * cfg.topl;
     const int cs = cfg.wt > 1 ? cfg.wt - 1 : 0;
@@ -101,8 +101,10 @@ static RefSearch ref_search(const VideoTensor& q, const VideoTensor& k, const Fl
     const RefCfg c = rc(cfg);
     if (ref_search_fwd(q.t, q.h, q.w, q.f, q.data.data(), k.data.data(), ff.data.data(),
                        bf.data.data(), &c, 0, 0, r.sims.data(), r.offsets.data(), r.centers.data(),
-                       r.chains.data()) != 0)
-        std::printf("  reference search failed: %s\n", ref_last_error());
+                       r.chains.data()) != 0) {
+        if (!quiet) std::printf("  reference search failed: %s\n", ref_last_error());
+        r.sims.clear();
+    }
     return r;
 }
 
@@ -161,7 +163,11 @@ int main() {
             SearchConfig probe = cfg;
             probe.topl = std::min(cfg.topl + 1, cfg.window_slots());
             const RefSearch r = ref_search(q, k, ff, bf, cfg);
-            const RefSearch rp = ref_search(q, k, ff, bf, probe);
+            RefSearch rp = ref_search(q, k, ff, bf, probe, true);
+            if (rp.sims.empty()) {  // one more rank does not exist for every query
+                rp = r;
+                probe = cfg;
+            }
             for (std::int64_t row = 0; row < a.sims.rows; ++row) {
                 bool near = false;
                 for (int li = 0; li + 1 < probe.topl; ++li) {

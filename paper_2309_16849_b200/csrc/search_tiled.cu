@@ -19,6 +19,8 @@
 //  * Epilogue: G-lane merge keyed on (value desc, slot asc), emit_row (search.cpp:207-234),
 //    chains, and softmax_rows (aggregate.cpp:16-37) when weights are requested.
 // The full ws^2 (2wt+1) score tensor is never materialised, in HBM or shared memory.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -112,8 +114,8 @@ __device__ __forceinline__ void write_off_frame(float* grid, int64_t row, int fp
     for (int s = gl; s < W * W; s += G) g[s] = -INFINITY;
 }
 
-template <int P, int W, int VEC, int G, int KMAX, int METRIC>
-__global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB>
+__global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G, KMAX>;
     using V = Vec<VEC>;
     constexpr int HP = C::HP, HW = C::HW, R = C::R;
@@ -352,15 +354,31 @@ __global__ void __launch_bounds__(128) search_tiled_kernel(TiledSearch a) {
     }
 }
 
-template <int P, int W, int VEC, int G, int KMAX>
-int launch_cfg(const TiledSearch& s, cudaStream_t st) {
+// Occupancy variant: MINB resident CTAs per SM (3 -> <=168 regs, 4 -> <=128 regs).
+// $SNLS_TILED_MINB selects it at run time (experiments); default 3.
+inline int tiled_minb() {
+    static const int v = [] {
+        const char* e = std::getenv("SNLS_TILED_MINB");
+        return (e && std::atoi(e) == 4) ? 4 : 3;
+    }();
+    return v;
+}
+
+template <int P, int W, int VEC, int G, int KMAX, int MINB>
+int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     using C = TiledCfg<P, W, VEC, G, KMAX>;
     const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
     if (s.metric == SNLS_METRIC_IP)
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB><<<blocks, 32 * C::WARPS, 0, st>>>(s);
     else
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB><<<blocks, 32 * C::WARPS, 0, st>>>(s);
     return 1;
+}
+
+template <int P, int W, int VEC, int G, int KMAX>
+int launch_cfg(const TiledSearch& s, cudaStream_t st) {
+    if (P == 3 && G == 8 && tiled_minb() == 4) return launch_cfg_b<P, W, VEC, G, KMAX, 4>(s, st);
+    return launch_cfg_b<P, W, VEC, G, KMAX, 3>(s, st);
 }
 
 template <int P, int W, int KMAX>

@@ -371,144 +371,129 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 }
 
 // ---- query-centric wpsum ----------------------------------------------------------------
-// A CTA owns a TY x TX output tile (all channels, accumulated in shared memory).  Every query
-// whose write set (footprint + stride-cell remainder, aggregate.cpp:80-100) meets the tile is
-// visited once per neighbour l: its (ps+1)^2 raw V block is read ONCE (coalesced float4 per
-// lane) and all ps^2 bilinear samples are formed from it -- (ps+1)^2 loads instead of the
-// 4*ps^2 a per-pixel gather issues.  Deterministic without atomics: queries are processed in
-// 4 colour classes (grid row / column parity); a query's write set lies within s0-1 of it, so
-// two queries of one class never write the same pixel.  Per pixel the sum order is
-// (class, query, neighbour) -- fixed, but not the reference's, so equal to it to rounding.
+// A CTA owns a TY x TX output tile of one frame (all channels).  Phase A: every query whose
+// write set (footprint + stride-cell remainder, aggregate.cpp:80-100) can meet the tile is
+// handled by one group of G lanes (float4 of channels each); for each neighbour l it reads the
+// (ps+1)^2 raw V block ONCE and accumulates all ps^2 softmax-weighted bilinear samples in
+// registers -- (ps+1)^2 loads per (query, l) instead of the 4*ps^2 of a per-pixel gather --
+// then parks the ps^2 patch in shared memory.  Phase B: each output pixel sums the parked
+// patches of its contributing units in the reference's fixed order (footprint py, px
+// ascending, then the owning query's cell completion; aggregate.cpp:156-188), divides by the
+// count and writes once.  Deterministic, no atomics, one barrier.
 template <int P, int G, int TY, int TX>
 __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
                                                           int32_t* __restrict__ counts) {
-    extern __shared__ float4 s_acc[];  // TY*TX*G float4, then TY*TX int counts
-    int* s_cnt = reinterpret_cast<int*>(s_acc + TY * TX * G);
-    constexpr int HP = P / 2, NQG = 256 / G;  // query groups per CTA
+    extern __shared__ float4 s_patch[];  // [query][P*P][G]
+    constexpr int HP = P / 2, NQG = 256 / G;
     const int H = a.d.h, W = a.d.w, st = a.d.stride0;
     const int tiles_x = (W + TX - 1) / TX, tiles_y = (H + TY - 1) / TY;
     const int tx0 = (blockIdx.x % tiles_x) * TX;
     const int ty0 = ((blockIdx.x / tiles_x) % tiles_y) * TY;
     const int ti = blockIdx.x / (tiles_x * tiles_y);
-    for (int i = threadIdx.x; i < TY * TX * G; i += 256) s_acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = threadIdx.x; i < TY * TX; i += 256) s_cnt[i] = 0;
-    // queries whose write extent [q-s0+1, q+s0-1] meets the tile
-    const int gy_lo = max(0, (ty0 - st + 1 + st - 1) / st - 0);
-    const int gy_hi = min(a.d.nh - 1, (ty0 + TY - 1 + st - 1) / st);
-    const int gx_lo = max(0, (tx0 - st + 1 + st - 1) / st - 0);
-    const int gx_hi = min(a.d.nw - 1, (tx0 + TX - 1 + st - 1) / st);
+    // any query writing inside the tile lies within s0-1 of it
+    const int gy_lo = ty0 / st, gy_hi = min(a.d.nh - 1, (ty0 + TY - 1 + st - 1) / st);
+    const int gx_lo = tx0 / st, gx_hi = min(a.d.nw - 1, (tx0 + TX - 1 + st - 1) / st);
+    const int nqx = gx_hi - gx_lo + 1, nq = (gy_hi - gy_lo + 1) * nqx;
     const int grp = threadIdx.x / G, gl = threadIdx.x % G;
-    const float4* vbase = reinterpret_cast<const float4*>(a.v) + gl;
     const unsigned row4 = unsigned(W) * G;
-    const float4* vframe0 = vbase;  // frame offset applied per neighbour
-    __syncthreads();
-    for (int cls = 0; cls < 4; ++cls) {
-        const int py0 = cls >> 1, px0 = cls & 1;
-        // grid indices of this class inside [gy_lo, gy_hi] x [gx_lo, gx_hi]
-        const int cy0 = gy_lo + ((py0 - gy_lo) & 1), cx0 = gx_lo + ((px0 - gx_lo) & 1);
-        const int ncy = cy0 > gy_hi ? 0 : (gy_hi - cy0) / 2 + 1;
-        const int ncx = cx0 > gx_hi ? 0 : (gx_hi - cx0) / 2 + 1;
-        for (int qi = grp; qi < ncy * ncx; qi += NQG) {
-            const int gy = cy0 + 2 * (qi / ncx), gx = cx0 + 2 * (qi % ncx);
-            const int qy = gy * st, qx = gx * st;
-            const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx;
-            float4 acc[P][P];
+    const float4* vbase = reinterpret_cast<const float4*>(a.v) + gl;
+
+    for (int qi = grp; qi < nq; qi += NQG) {
+        const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
+        const int qy = gy * st, qx = gx * st;
+        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx;
+        float4 acc[P][P];
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int j = 0; j < P; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int l = 0; l < a.topl; ++l) {
+            const size_t e = size_t(row) * a.topl + l;
+            const float* o = a.offsets + e * 3;
+            int kt = ti + int(roundf(__ldg(o)));
+            if (kt < 0 || kt >= a.d.t) {  // "offsets leave the clip" (aggregate.cpp:108-109)
+                latch(a.err, kErrWpsum);
+                kt = ti;
+            }
+            const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+            const float fly = floorf(oy), flx = floorf(ox);
+            const float fy = oy - fly, fx = ox - flx;
+            const float wv = __ldg(a.weights + e);
+            const float w00 = wv * ((1.f - fy) * (1.f - fx)), w01 = wv * ((1.f - fy) * fx);
+            const float w10 = wv * (fy * (1.f - fx)), w11 = wv * (fy * fx);
+            // sample (i, j) sits between raw rows by+i, by+i+1 and cols bx+j, bx+j+1
+            const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+            const float4* vf = vbase + size_t(kt) * H * row4;
+            float4 blk[P + 1][P + 1];
+            if (by >= 0 && by + P < H && bx >= 0 && bx + P < W) {
+                const float4* p0 = vf + (unsigned(by) * row4 + unsigned(bx) * G);
+#pragma unroll
+                for (int i = 0; i <= P; ++i)
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) blk[i][j] = __ldg(p0 + i * row4 + j * G);
+            } else {  // reflected border taps (tensor.cpp:31-48)
+#pragma unroll
+                for (int i = 0; i <= P; ++i) {
+                    const unsigned r = unsigned(reflect_near(by + i, H)) * row4;
+#pragma unroll
+                    for (int j = 0; j <= P; ++j)
+                        blk[i][j] = __ldg(vf + (r + unsigned(reflect_near(bx + j, W)) * G));
+                }
+            }
 #pragma unroll
             for (int i = 0; i < P; ++i)
 #pragma unroll
-                for (int j = 0; j < P; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int l = 0; l < a.topl; ++l) {
-                const size_t e = size_t(row) * a.topl + l;
-                const float* o = a.offsets + e * 3;
-                int kt = ti + int(roundf(__ldg(o)));
-                if (kt < 0 || kt >= a.d.t) {
-                    latch(a.err, kErrWpsum);
-                    kt = ti;
+                for (int j = 0; j < P; ++j) {
+                    float4& c = acc[i][j];
+                    const float4 &A = blk[i][j], &B = blk[i][j + 1], &C = blk[i + 1][j], &D = blk[i + 1][j + 1];
+                    c.x = fmaf(w11, D.x, fmaf(w10, C.x, fmaf(w01, B.x, fmaf(w00, A.x, c.x))));
+                    c.y = fmaf(w11, D.y, fmaf(w10, C.y, fmaf(w01, B.y, fmaf(w00, A.y, c.y))));
+                    c.z = fmaf(w11, D.z, fmaf(w10, C.z, fmaf(w01, B.z, fmaf(w00, A.z, c.z))));
+                    c.w = fmaf(w11, D.w, fmaf(w10, C.w, fmaf(w01, B.w, fmaf(w00, A.w, c.w))));
                 }
-                const float oy = __ldg(o + 1), ox = __ldg(o + 2);
-                const float fly = floorf(oy), flx = floorf(ox);
-                const float fy = oy - fly, fx = ox - flx;
-                const float wv = __ldg(a.weights + e);
-                const float w00 = wv * ((1.f - fy) * (1.f - fx)), w01 = wv * ((1.f - fy) * fx);
-                const float w10 = wv * (fy * (1.f - fx)), w11 = wv * (fy * fx);
-                // raw block rows by .. by+P, cols bx .. bx+P (sample (i,j) = block (i..i+1, j..j+1))
-                const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
-                const float4* vf = vframe0 + size_t(kt) * H * row4;
-                unsigned xo[P + 1];
-                const bool inx = bx >= 0 && bx + P < W;
-#pragma unroll
-                for (int j = 0; j <= P; ++j) xo[j] = unsigned(inx ? bx + j : reflect_near(bx + j, W)) * G;
-                float4 top[P + 1];
-                {
-                    const unsigned r = unsigned(reflect_near(by, H)) * row4;
-#pragma unroll
-                    for (int j = 0; j <= P; ++j) top[j] = __ldg(vf + (r + xo[j]));
-                }
-#pragma unroll
-                for (int i = 0; i < P; ++i) {
-                    const unsigned r = unsigned(reflect_near(by + i + 1, H)) * row4;
-                    float4 bot[P + 1];
-#pragma unroll
-                    for (int j = 0; j <= P; ++j) bot[j] = __ldg(vf + (r + xo[j]));
-#pragma unroll
-                    for (int j = 0; j < P; ++j) {
-                        float4& c = acc[i][j];
-                        c.x = fmaf(w11, bot[j + 1].x, fmaf(w10, bot[j].x, fmaf(w01, top[j + 1].x, fmaf(w00, top[j].x, c.x))));
-                        c.y = fmaf(w11, bot[j + 1].y, fmaf(w10, bot[j].y, fmaf(w01, top[j + 1].y, fmaf(w00, top[j].y, c.y))));
-                        c.z = fmaf(w11, bot[j + 1].z, fmaf(w10, bot[j].z, fmaf(w01, top[j + 1].z, fmaf(w00, top[j].z, c.z))));
-                        c.w = fmaf(w11, bot[j + 1].w, fmaf(w10, bot[j].w, fmaf(w01, top[j + 1].w, fmaf(w00, top[j].w, c.w))));
-                    }
-#pragma unroll
-                    for (int j = 0; j <= P; ++j) top[j] = bot[j];
-                }
-            }
-            // scatter into the tile: footprint, then the stride-cell remainder (clamped sample)
-            const int a_c = (st - 1) / 2;
-            const int cly = gy == 0 ? 0 : qy - a_c, chy = gy == a.d.nh - 1 ? H - 1 : qy + (st - 1 - a_c);
-            const int clx = gx == 0 ? 0 : qx - a_c, chx = gx == a.d.nw - 1 ? W - 1 : qx + (st - 1 - a_c);
-            const int ylo = max(ty0, min(qy - HP, cly)), yhi = min(min(ty0 + TY - 1, H - 1), max(qy + HP, chy));
-            const int xlo = max(tx0, min(qx - HP, clx)), xhi = min(min(tx0 + TX - 1, W - 1), max(qx + HP, chx));
-            for (int y = ylo; y <= yhi; ++y) {
-                const bool foot_y = abs(y - qy) <= HP, cell_y = y >= cly && y <= chy;
-                if (!foot_y && !cell_y) continue;
-                const int si = min(max(y - qy, -HP), HP) + HP;
-                for (int x = xlo; x <= xhi; ++x) {
-                    const bool foot = foot_y && abs(x - qx) <= HP;
-                    const bool cell = cell_y && x >= clx && x <= chx;
-                    if (!foot && !cell) continue;
-                    const int sj = min(max(x - qx, -HP), HP) + HP;
-                    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                    for (int i = 0; i < P; ++i)
-#pragma unroll
-                        for (int j = 0; j < P; ++j)
-                            if (i == si && j == sj) sv = acc[i][j];
-                    const int pix = (y - ty0) * TX + (x - tx0);
-                    float4& d = s_acc[pix * G + gl];
-                    d.x += sv.x;
-                    d.y += sv.y;
-                    d.z += sv.z;
-                    d.w += sv.w;
-                    if (gl == 0) s_cnt[pix] += 1;
-                }
-            }
         }
-        __syncthreads();
+        float4* dst = s_patch + size_t(qi) * P * P * G + gl;
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int j = 0; j < P; ++j) dst[(i * P + j) * G] = acc[i][j];
     }
-    // normalise and write the tile (aggregate.cpp:193-198)
-    for (int i = threadIdx.x; i < TY * TX * G; i += 256) {
-        const int pix = i / G, c = i % G;
+    __syncthreads();
+
+    // phase B: fixed-order gather from the parked patches
+    for (int idx = threadIdx.x; idx < TY * TX * G; idx += 256) {
+        const int pix = idx / G, c = idx % G;
         const int y = ty0 + pix / TX, x = tx0 + pix % TX;
         if (y >= H || x >= W) continue;
-        const int cnt = s_cnt[pix];
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+        int cnt = 0;
+        auto add = [&](int gy, int gx, int si, int sj) {
+            const float4 v = s_patch[(size_t((gy - gy_lo) * nqx + (gx - gx_lo)) * P * P + si * P + sj) * G + c];
+            sum.x += v.x;
+            sum.y += v.y;
+            sum.z += v.z;
+            sum.w += v.w;
+            ++cnt;
+        };
+        const AxisUnits uy = axis_units(y, st, HP, (a.d.nh - 1) * st);
+        const AxisUnits ux = axis_units(x, st, HP, (a.d.nw - 1) * st);
+        for (int iy = 0; iy < uy.n; ++iy) {
+            const int py = iy == 0 ? uy.p0 : uy.p1;
+            for (int ix = 0; ix < ux.n; ++ix) {
+                const int px = ix == 0 ? ux.p0 : ux.p1;
+                add((y - py) / st, (x - px) / st, py + HP, px + HP);
+            }
+        }
+        const int gy = owner_index(y, st, a.d.nh), gx = owner_index(x, st, a.d.nw);
+        if (abs(y - gy * st) > HP || abs(x - gx * st) > HP)
+            add(gy, gx, clampi(y - gy * st, HP) + HP, clampi(x - gx * st, HP) + HP);
         const size_t gp = (size_t(ti) * H + y) * W + x;
         if (cnt <= 0) {
             latch(a.err, kErrWpsum);
             continue;
         }
-        const float4 v = s_acc[i];
         const float fc = float(cnt);
-        reinterpret_cast<float4*>(out + gp * a.d.f)[c] = make_float4(v.x / fc, v.y / fc, v.z / fc, v.w / fc);
+        reinterpret_cast<float4*>(out + gp * a.d.f)[c] = make_float4(sum.x / fc, sum.y / fc, sum.z / fc, sum.w / fc);
         if (c == 0 && counts) counts[gp] = cnt;
     }
 }
@@ -516,7 +501,12 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
 template <int P, int G>
 int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     constexpr int TY = 16, TX = 16;
-    const size_t smem = size_t(TY) * TX * G * sizeof(float4) + size_t(TY) * TX * sizeof(int);
+    const int s0 = a.d.stride0;
+    // grid rows meeting a tile aligned to TY (tiles start at multiples of TY)
+    const int nqy = (TY + s0 - 2) / s0 + (TY % s0 == 0 ? 1 : 2);
+    const int nqx = (TX + s0 - 2) / s0 + (TX % s0 == 0 ? 1 : 2);
+    const int nq = nqy * nqx;
+    const size_t smem = size_t(nq) * P * P * G * sizeof(float4);
     if (smem > 200 * 1024) return 0;
     cudaFuncSetAttribute(wpsum_query_kernel<P, G, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));

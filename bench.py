@@ -42,6 +42,12 @@ WORKLOADS = {
     "c2": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
                beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0,
                name="c2: 5x128x128x64, ws9 wt2 ps7 k10 ip s0=4"),
+    # BASELINE configs[4]: single video T=64 C=64 H=W=512 ws=9 wt=2 ps=3 k=10, frame-sharded
+    # across ranks with a wt-frame NCCL halo (per-frame seeds 500*1000+t)
+    "c5": dict(T=64, H=512, W=512, C=64, ws=9, wt=2, ps=3, topl=10, metric="l2", stride0=2,
+               beta=1.0 / 576, vid_seed=500, ff_seed=501, bf_seed=502, flow_mag=2.0,
+               sharded=True,
+               name="c5: one 64x512x512x64 video, ws9 wt2 ps3 k10 L2 s0=2, frame-sharded + halo"),
 }
 
 
@@ -155,6 +161,21 @@ def dist_env():
     return rank, world, local
 
 
+def make_frames(S, wl, t0, t1):
+    """Frames [t0, t1) of the c5 video, flows and video from per-frame seeds."""
+    import numpy as np
+
+    H, W, C = wl["H"], wl["W"], wl["C"]
+    vid = np.stack([S.uniform_fill(wl["vid_seed"] * 1000 + t, -1.0, 1.0, H * W * C).reshape(H, W, C)
+                    for t in range(t0, t1)])
+    m = wl["flow_mag"]
+    ff = np.stack([S.uniform_fill(wl["ff_seed"] * 1000 + t, -m, m, H * W * 2).reshape(H, W, 2)
+                   for t in range(t0, t1)])
+    bf = np.stack([S.uniform_fill(wl["bf_seed"] * 1000 + t, -m, m, H * W * 2).reshape(H, W, 2)
+                   for t in range(t0, t1)])
+    return vid, ff, bf
+
+
 def make_inputs(S, wl, b):
     import numpy as np
 
@@ -180,25 +201,41 @@ def run_ours(args, wl):
     rows = model["rows"]
     cfg = S.SearchConfig(ws=wl["ws"], wt=wl["wt"], ps=wl["ps"], stride0=wl["stride0"],
                          stride1=1.0, topl=wl["topl"], metric=wl["metric"], softmax_scale=wl["beta"])
-    vid_h, ff_h, bf_h = make_inputs(S, wl, rank)
-    vid = torch.from_numpy(vid_h).to(dev)
-    ff = torch.from_numpy(ff_h).to(dev)
-    bf = torch.from_numpy(bf_h).to(dev)
+    sharded = wl.get("sharded", False)
+    if sharded:  # frame sharding: own frames [a, b), halo frames from the neighbours (NCCL)
+        from paper_2309_16849_b200 import shard as SH
+
+        plan = SH.plan(wl["T"], world, rank, wl["wt"])
+        vid_h, ff_h, bf_h = make_frames(S, wl, plan.a, plan.b)
+        frames = (plan.t0, plan.t1)
+        rows = (plan.b - plan.a) * (rows // wl["T"])
+    else:
+        vid_h, ff_h, bf_h = make_inputs(S, wl, rank)
+        frames = None
+    own_vid = torch.from_numpy(vid_h).to(dev)
+    own_ff = torch.from_numpy(ff_h).to(dev)
+    own_bf = torch.from_numpy(bf_h).to(dev)
+    vid, ff, bf = own_vid, own_ff, own_bf
+    if sharded:  # slab buffers (the exchange refills them every step when world > 1)
+        vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
     stream = torch.cuda.current_stream(dev)
     ctx = S.context(local)
     L = wl["topl"]
     sims = torch.empty((rows, L), device=dev)
     offs = torch.empty((rows, L, 3), device=dev)
     wts = torch.empty((rows, L), device=dev)
-    out = torch.empty_like(vid)
-    counts = torch.empty(vid.shape[:3], device=dev, dtype=torch.int32)
+    out = torch.empty_like(own_vid)
+    counts = torch.empty(own_vid.shape[:3], device=dev, dtype=torch.int32)
     flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
 
     def step():
+        nonlocal vid, ff, bf
+        if sharded and world > 1:  # the data path's only communication: the wt-frame halo
+            vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
         S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
-                              out=(sims, offs, None, wts))
+                              out=(sims, offs, None, wts), frames=frames)
         ev_mid.record(stream)
-        S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts))
+        S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
 
     # correctness gate before timing: device error latch must be clean
     ev_mid = torch.cuda.Event(enable_timing=True)
@@ -250,15 +287,18 @@ def run_ours(args, wl):
     sims_p = torch.empty((rows, L)).pin_memory()
     offs_p = torch.empty((rows, L, 3)).pin_memory()
     out_p = torch.empty(vid_h.shape).pin_memory()
-    vd, ffd, bfd = torch.empty_like(vid), torch.empty_like(ff), torch.empty_like(bf)
+    vd, ffd, bfd = torch.empty_like(own_vid), torch.empty_like(own_ff), torch.empty_like(own_bf)
 
     def e2e_step():
         vd.copy_(vid_p, non_blocking=True)
         ffd.copy_(ff_p, non_blocking=True)
         bfd.copy_(bf_p, non_blocking=True)
-        S.shifted_nls_forward(vd, vd, ffd, bfd, cfg, ctx=ctx, check=False,
-                              out=(sims, offs, None, wts))
-        S.wpsum(vd, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts))
+        v2, f2, b2 = vd, ffd, bfd
+        if sharded:
+            v2, f2, b2 = SH.exchange(vd, plan), SH.exchange(ffd, plan), SH.exchange(bfd, plan)
+        S.shifted_nls_forward(v2, v2, f2, b2, cfg, ctx=ctx, check=False,
+                              out=(sims, offs, None, wts), frames=frames)
+        S.wpsum(v2, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
         sims_p.copy_(sims, non_blocking=True)
         offs_p.copy_(offs, non_blocking=True)
         out_p.copy_(out, non_blocking=True)
@@ -289,12 +329,14 @@ def run_ours(args, wl):
             dist.barrier()
             dist.destroy_process_group()
         return
+    total_rows = model["rows"] if sharded else rows * world
     P, peak_src = peaks()
     sm_max = float(P.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak_tflops = nsm * 128 * 2 * sm_max * 1e6 / 1e12
     t_search = tot_search / args.steps / 1e3
-    achieved = 2.0 * model["search_instr"] / t_search / 1e12
+    share = rows / model["rows"]  # this rank's fraction of the video (frame sharding)
+    achieved = 2.0 * model["search_instr"] * share / t_search / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -304,7 +346,7 @@ def run_ours(args, wl):
             traffic = None
     result = {
         "metric": METRIC,
-        "value": rows * world / (ms_per_step / 1e3),
+        "value": total_rows / (ms_per_step / 1e3),
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
@@ -312,12 +354,15 @@ def run_ours(args, wl):
         "ms_per_step": ms_per_step,
         "ms_per_video": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic: reference UniformStream video U[-1,1) (Q=K=V) and flows U[-2,2)",
-        "config": {"workload": wl["name"], "videos_per_gpu": 1, "queries_per_video": rows,
-                   "parallelism": f"batch-sharded x{world} (no collective)",
+        "config": {"workload": wl["name"],
+                   "videos_per_gpu": 1 if not sharded else f"1/{world} (frames {plan.a}..{plan.b - 1} on rank 0)",
+                   "queries_per_gpu": rows,
+                   "parallelism": (f"frame-sharded x{world}, wt-frame halo via NCCL send/recv"
+                                   if sharded else f"batch-sharded x{world} (no collective)"),
                    "l2": "flushed (512 MB memset) between timed steps"},
         "breakdown_ms": {"search_topl_softmax": tot_search / args.steps,
                          "wpsum": statistics.mean(wpsum_ms)},
@@ -326,8 +371,8 @@ def run_ours(args, wl):
                      "frac": achieved / fp32_peak_tflops, "traffic": traffic,
                      "algorithmic": f"{model['search_instr']:.4g} FMA-pipe instr/video x2 flop",
                      "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x sm_max_mhz from {peak_src}",
-                     "hbm_frac": model["bytes_search"] / t_search / 1e9 / float(P.get("hbm_gbs", 6650))},
-        "e2e": {"value": rows * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                     "hbm_frac": model["bytes_search"] * share / t_search / 1e9 / float(P.get("hbm_gbs", 6650))},
+        "e2e": {"value": total_rows / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk,

@@ -109,6 +109,14 @@ int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const
                     const float* k, const float* fflow, const float* bflow, int mode,
                     float* sims, float* offsets, float* chains, float* weights);
 
+/* Frame-range form used by frame sharding: only the query rows of frames [t0, t1) are
+ * searched (outputs hold those rows, rows = (t1-t0)*nh*nw); q/k/flows are the full `dims.t`
+ * frames the caller holds (a shard's slab incl. its wt-frame halo), and key frames outside
+ * [0, dims.t) are off-clip exactly as in search.cpp:300. */
+int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                           const float* q, const float* k, const float* fflow, const float* bflow,
+                           int mode, float* sims, float* offsets, float* chains, float* weights);
+
 /* The pre-selection score grid rows x window_slots (-inf on off-clip frames) and its
  * offsets rows x window_slots x 3, as full_grid_forward builds it (search.cpp:351-376). */
 int snls_search_grid(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
@@ -140,6 +148,13 @@ int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const flo
  * out T x H x W x F, counts T x H x W (the AggTape, aggregate.hpp:27-36). */
 int snls_wpsum_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
                    const float* weights, const float* offsets, float* out, int32_t* counts);
+
+/* Frame-range form: output frames [t0, t1) only (out (t1-t0) x H x W x F, counts
+ * (t1-t0) x H x W), from the weights/offsets of those frames' query rows; v holds all
+ * dims.t frames (wpsum writes only into the query's own frame, aggregate.cpp:197-198). */
+int snls_wpsum_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* v, const float* weights, const float* offsets, float* out,
+                          int32_t* counts);
 
 /* Replaces snls::gather_stack (aggregate.hpp:71-73; aggregate.cpp:285-347).
  * out L x T x H x W x F. */

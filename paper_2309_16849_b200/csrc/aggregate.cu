@@ -79,7 +79,7 @@ __device__ int gather_pixel(const AggArgs& a, int ti, int y, int x, int l0, int 
         for (int px = -half; px <= half; ++px) {
             const int qx = x - px;
             if (qx < 0 || qx > qmax_x || qx % st != 0) continue;
-            const int64_t row = (int64_t(ti) * a.d.nh + qy / st) * a.d.nw + qx / st;
+            const int64_t row = (int64_t(ti) * a.d.nh + qy / st) * a.d.nw + qx / st - a.d.row0;
             if (!add_unit<VEC>(a, row, ti, qy, qx, py, px, l0, l1, c, acc)) return -1;
             ++cnt;
         }
@@ -87,7 +87,7 @@ __device__ int gather_pixel(const AggArgs& a, int ti, int y, int x, int l0, int 
     const int qy = owner_index(y, st, a.d.nh) * st;
     const int qx = owner_index(x, st, a.d.nw) * st;
     if (abs(y - qy) > half || abs(x - qx) > half) {
-        const int64_t row = (int64_t(ti) * a.d.nh + qy / st) * a.d.nw + qx / st;
+        const int64_t row = (int64_t(ti) * a.d.nh + qy / st) * a.d.nw + qx / st - a.d.row0;
         if (!add_unit<VEC>(a, row, ti, qy, qx, clampi(y - qy, half), clampi(x - qx, half), l0,
                            l1, c, acc))
             return -1;
@@ -100,14 +100,14 @@ template <int VEC>
 __global__ void __launch_bounds__(256) wpsum_kernel(AggArgs a, float* __restrict__ out,
                                                     int32_t* __restrict__ counts) {
     const int groups = a.d.f / VEC;
-    const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
+    const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= npix * groups) return;
-    const int64_t pix = idx / groups;
+    const int64_t pix = idx / groups;  // local to the frame range
     const int c = int(idx % groups) * VEC;
     const int x = int(pix % a.d.w);
     const int y = int((pix / a.d.w) % a.d.h);
-    const int ti = int(pix / (int64_t(a.d.w) * a.d.h));
+    const int ti = a.d.t0 + int(pix / (int64_t(a.d.w) * a.d.h));
     float acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) wpsum_kernel(AggArgs a, float* __restrict
 template <int VEC>
 __global__ void __launch_bounds__(256) gather_stack_kernel(AggArgs a, float* __restrict__ out) {
     const int groups = a.d.f / VEC;
-    const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
+    const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= npix * groups * a.topl) return;
     const int li = int(idx / (npix * groups));
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) gather_stack_kernel(AggArgs a, float* __r
     const int c = int(r % groups) * VEC;
     const int x = int(pix % a.d.w);
     const int y = int((pix / a.d.w) % a.d.h);
-    const int ti = int(pix / (int64_t(a.d.w) * a.d.h));
+    const int ti = a.d.t0 + int(pix / (int64_t(a.d.w) * a.d.h));
     float acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
@@ -191,7 +191,7 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int l = i % a.topl, qi = i / a.topl;
         const int gy = g.gy_lo + qi / g.nqx, gx = g.gx_lo + qi % g.nqx;
-        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx;
+        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx - a.d.row0;
         const size_t e = size_t(row) * a.topl + l;
         const float* o = a.offsets + e * 3;
         SampleDesc d;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
     const int tiles_x = (a.d.w + PPC - 1) / PPC;
     const int tx = blockIdx.x % tiles_x;
     const int y = (blockIdx.x / tiles_x) % a.d.h;
-    const int ti = blockIdx.x / (tiles_x * a.d.h);
+    const int ti = a.d.t0 + int(blockIdx.x / (tiles_x * a.d.h));
     const int x0 = tx * PPC;
     const TileGeom g = tile_geom(a, y, x0, PPC);
     build_descs(a, ti, g, s_desc, a.err, stack ? kErrStack : kErrWpsum);
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
         *reinterpret_cast<float4*>(out + pix * a.d.f + c) =
             make_float4(acc.x / fc, acc.y / fc, acc.z / fc, acc.w / fc);
     } else {
-        const size_t plane = size_t(a.d.t) * a.d.h * a.d.w * a.d.f;
+        const size_t plane = size_t(a.d.nt) * a.d.h * a.d.w * a.d.f;
         for (int l = 0; l < a.topl; ++l) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             gather_tiled<4>(a, s_desc, g, uy, y, x, l, l + 1, c, acc);
@@ -352,7 +352,7 @@ int launch_tiled_agg(const AggArgs& a, float* out, int32_t* counts, int stack, c
     if (smem > 200 * 1024) return 0;
     cudaFuncSetAttribute(wpsum_tiled_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int tiles_x = (a.d.w + PPC - 1) / PPC;
-    const unsigned blocks = unsigned(int64_t(a.d.t) * a.d.h * tiles_x);
+    const unsigned blocks = unsigned(int64_t(a.d.nt) * a.d.h * tiles_x);
     wpsum_tiled_kernel<G><<<blocks, 256, smem, st>>>(a, out, counts, stack);
     return 1;
 }
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
     const int tiles_x = (W + TX - 1) / TX, tiles_y = (H + TY - 1) / TY;
     const int tx0 = (blockIdx.x % tiles_x) * TX;
     const int ty0 = ((blockIdx.x / tiles_x) % tiles_y) * TY;
-    const int ti = blockIdx.x / (tiles_x * tiles_y);
+    const int ti = a.d.t0 + int(blockIdx.x / (tiles_x * tiles_y));
     // any query writing inside the tile lies within s0-1 of it
     const int gy_lo = ty0 / st, gy_hi = min(a.d.nh - 1, (ty0 + TY - 1 + st - 1) / st);
     const int gx_lo = tx0 / st, gx_hi = min(a.d.nw - 1, (tx0 + TX - 1 + st - 1) / st);
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
     for (int qi = grp; qi < nq; qi += NQG) {
         const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
         const int qy = gy * st, qx = gx * st;
-        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx;
+        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx - a.d.row0;
         float4 acc[P][P];
 #pragma unroll
         for (int i = 0; i < P; ++i)
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
         const int gy = owner_index(y, st, a.d.nh), gx = owner_index(x, st, a.d.nw);
         if (abs(y - gy * st) > HP || abs(x - gx * st) > HP)
             add(gy, gx, clampi(y - gy * st, HP) + HP, clampi(x - gx * st, HP) + HP);
-        const size_t gp = (size_t(ti) * H + y) * W + x;
+        const size_t gp = (size_t(ti - a.d.t0) * H + y) * W + x;  // local output pixel
         if (cnt <= 0) {
             latch(a.err, kErrWpsum);
             continue;
@@ -511,7 +511,7 @@ int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream
     cudaFuncSetAttribute(wpsum_query_kernel<P, G, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
     const int tiles = ((a.d.w + TX - 1) / TX) * ((a.d.h + TY - 1) / TY);
-    wpsum_query_kernel<P, G, TY, TX><<<unsigned(int64_t(a.d.t) * tiles), 256, smem, st>>>(a, out, counts);
+    wpsum_query_kernel<P, G, TY, TX><<<unsigned(int64_t(a.d.nt) * tiles), 256, smem, st>>>(a, out, counts);
     return 1;
 }
 
@@ -635,7 +635,7 @@ int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* we
 int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     if (int n = launch_wpsum_query_any(a, out, counts, st)) return n;
     if (int n = launch_tiled_agg_any(a, out, counts, 0, st)) return n;
-    const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
+    const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {
         const int64_t n = npix * (a.d.f / 4);
         wpsum_kernel<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, out, counts);
@@ -648,7 +648,7 @@ int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st)
 
 int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st) {
     if (int n = launch_tiled_agg_any(a, out, nullptr, 1, st)) return n;
-    const int64_t npix = int64_t(a.d.t) * a.d.h * a.d.w;
+    const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {
         const int64_t n = npix * (a.d.f / 4) * a.topl;
         gather_stack_kernel<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, out);

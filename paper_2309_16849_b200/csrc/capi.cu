@@ -90,9 +90,10 @@ int check_ctx(snls_ctx* ctx) {
 
 // fused_forward's underfull rule (search.cpp:317-325), decided from shapes alone: the
 // fewest valid frames any query frame sees, times ws^2.
-bool underfull(const snls_config* c, int t) {
+bool underfull(const snls_config* c, int t, int t0 = 0, int t1 = -1) {
     long long worst = -1;
-    for (int qt = 0; qt < t; ++qt) {
+    if (t1 < 0) t1 = t;
+    for (int qt = t0; qt < t1; ++qt) {
         const int lo = qt - c->wt < 0 ? 0 : qt - c->wt;
         const int hi = qt + c->wt > t - 1 ? t - 1 : qt + c->wt;
         const long long valid = (long long)(hi - lo + 1) * c->ws * c->ws;
@@ -303,12 +304,20 @@ static int search_common_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims
 int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
                     const float* k, const float* ff, const float* bf, int mode, float* sims,
                     float* offsets, float* chains, float* weights) {
+    return snls_search_fwd_frames(ctx, cfg, dims, 0, dims.t, q, k, ff, bf, mode, sims, offsets,
+                                  chains, weights);
+}
+
+int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                           const float* q, const float* k, const float* ff, const float* bf,
+                           int mode, float* sims, float* offsets, float* chains, float* weights) {
     if (int rc = search_common_checks(ctx, cfg, dims, q, k, ff, bf)) return rc;
     if (!sims || !offsets) return fail(SNLS_EARG, "search: null output");
-    if (underfull(cfg, dims.t))
+    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "search: empty or invalid frame range");
+    if (underfull(cfg, dims.t, t0, t1))
         return fail(SNLS_ECONFIG, "search: topl exceeds the valid window entries of some query");
     DeviceGuard g(ctx->device);
-    const Dims d = make_dims(dims, cfg->stride0);
+    const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     const int64_t nflow = int64_t(dims.t) * dims.h * dims.w * 2;
     int launched = launch_flows_check(ff, bf, nflow, ctx->err, ctx->stream);
     const float beta = float(cfg->softmax_scale);
@@ -455,10 +464,18 @@ static int agg_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
 
 int snls_wpsum_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,
                    const float* weights, const float* offsets, float* out, int32_t* counts) {
+    return snls_wpsum_fwd_frames(ctx, cfg, dims, 0, dims.t, v, weights, offsets, out, counts);
+}
+
+int snls_wpsum_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* v, const float* weights, const float* offsets, float* out,
+                          int32_t* counts) {
     if (int rc = agg_checks(ctx, cfg, dims, v, weights, offsets)) return rc;
     if (!out) return fail(SNLS_EARG, "wpsum: null output");
+    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "wpsum: empty or invalid frame range");
     DeviceGuard g(ctx->device);
-    AggArgs a{v, weights, offsets, make_dims(dims, cfg->stride0), cfg->ps, cfg->topl, ctx->err};
+    AggArgs a{v, weights, offsets, restrict_frames(make_dims(dims, cfg->stride0), t0, t1), cfg->ps,
+              cfg->topl, ctx->err};
     return after_launch(ctx, launch_wpsum(a, out, counts, ctx->stream), "snls_wpsum_fwd");
 }
 

@@ -23,10 +23,16 @@ enum : int {
     kErrTopl = 32,      // "top_l: some row has fewer than L valid entries" search.cpp:466
 };
 
+// Video dims plus the query/output FRAME RANGE [t0, t0+nt) being processed.  `rows` counts
+// the query rows of that range and kernels index outputs by the local row (global row -
+// row0); `t` stays the full clip length, which decides which key frames exist
+// (search.cpp:300).  The default range is the whole clip.
 struct Dims {
     int t, h, w, f;
     int nh, nw, stride0;
     int64_t rows;
+    int t0, nt;
+    int64_t row0;
 };
 
 __host__ __device__ inline Dims make_dims(snls_dims d, int stride0) {
@@ -39,7 +45,18 @@ __host__ __device__ inline Dims make_dims(snls_dims d, int stride0) {
     r.nh = (d.h - 1) / stride0 + 1;
     r.nw = (d.w - 1) / stride0 + 1;
     r.rows = int64_t(d.t) * r.nh * r.nw;
+    r.t0 = 0;
+    r.nt = d.t;
+    r.row0 = 0;
     return r;
+}
+
+__host__ __device__ inline Dims restrict_frames(Dims d, int t0, int t1) {
+    d.t0 = t0;
+    d.nt = t1 - t0;
+    d.row0 = int64_t(t0) * d.nh * d.nw;
+    d.rows = int64_t(d.nt) * d.nh * d.nw;
+    return d;
 }
 
 // tensor.cpp:23-29: period-2(n-1) mirror, any magnitude; n == 1 maps to 0.
@@ -63,8 +80,9 @@ __device__ __forceinline__ int reflect_near(int i, int n) {
 }
 
 // search.cpp:52-57
-__device__ __forceinline__ void row_coords(const Dims& d, int64_t row, int& qt, int& qy,
+__device__ __forceinline__ void row_coords(const Dims& d, int64_t local_row, int& qt, int& qy,
                                            int& qx) {
+    const int64_t row = local_row + d.row0;
     qx = int(row % d.nw) * d.stride0;
     const int64_t r = row / d.nw;
     qy = int(r % d.nh) * d.stride0;

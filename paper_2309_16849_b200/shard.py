@@ -1,0 +1,109 @@
+"""Frame sharding of one video across ranks (BASELINE configs[4]).
+
+A query at frame t only reads key/value frames t-wt .. t+wt and the flow frames between
+(search.cpp:84-101, 300), and wpsum writes only into the query's own frame
+(aggregate.cpp:197-198).  So rank r owns query frames [a, b) and needs the slab
+[lo, hi) = [a-wt, b+wt) ∩ [0, T) of K/V/flows: the wt-frame halo on each side comes from the
+neighbouring owners by point-to-point send/recv -- NCCL over NVLink on GPUs, gloo in the
+CPU tests -- and no other collective touches the data path.  Searching the slab with query
+rows restricted to [a-lo, b-lo) (snls_search_fwd_frames) gives exactly the rows the
+unsharded search gives: frames outside the slab are either off the clip or out of reach.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    rank: int
+    world: int
+    T: int
+    wt: int
+    a: int   # owned query frames [a, b)
+    b: int
+    lo: int  # slab frames [lo, hi)
+    hi: int
+
+    @property
+    def t0(self) -> int:  # owned frames inside the slab
+        return self.a - self.lo
+
+    @property
+    def t1(self) -> int:
+        return self.b - self.lo
+
+
+def owned_range(T: int, world: int, rank: int):
+    """Balanced contiguous split of T frames over `world` ranks."""
+    per, rem = divmod(T, world)
+    a = rank * per + min(rank, rem)
+    return a, a + per + (1 if rank < rem else 0)
+
+
+def plan(T: int, world: int, rank: int, wt: int) -> ShardPlan:
+    if world > T:
+        raise ValueError("frame sharding needs at least one frame per rank")
+    a, b = owned_range(T, world, rank)
+    return ShardPlan(rank, world, T, wt, a, b, max(0, a - wt), min(T, b + wt))
+
+
+def transfers(p: ShardPlan):
+    """(peer, frame range, 'send'|'recv') messages of rank p.rank, peers in ascending order.
+    A peer's frames that fall in my slab are received; my frames inside a peer's slab are sent.
+    Works for any shard length (halo may span several owners when b - a < wt)."""
+    out = []
+    for peer in range(p.world):
+        if peer == p.rank:
+            continue
+        pa, pb = owned_range(p.T, p.world, peer)
+        # frames I need from `peer`
+        lo, hi = max(p.lo, pa), min(p.hi, pb)
+        if lo < hi:
+            out.append((peer, (lo, hi), "recv"))
+        # frames `peer` needs from me
+        q = plan(p.T, p.world, peer, p.wt)
+        lo, hi = max(q.lo, p.a), min(q.hi, p.b)
+        if lo < hi:
+            out.append((peer, (lo, hi), "send"))
+    return out
+
+
+def exchange(local, p: ShardPlan, group=None):
+    """Assemble the slab [lo, hi) from `local` (the owned frames [a, b), frame-major tensor)
+    with one batched send/recv per (peer, direction).  Returns the slab tensor."""
+    import torch
+    import torch.distributed as dist
+
+    shape = (p.hi - p.lo,) + tuple(local.shape[1:])
+    slab = torch.empty(shape, dtype=local.dtype, device=local.device)
+    slab[p.a - p.lo:p.b - p.lo].copy_(local)
+    ops = []
+    for peer, (lo, hi), kind in transfers(p):
+        if kind == "recv":
+            ops.append(dist.P2POp(dist.irecv, slab[lo - p.lo:hi - p.lo], peer, group))
+        else:
+            ops.append(dist.P2POp(dist.isend, local[lo - p.a:hi - p.a].contiguous(), peer, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return slab
+
+
+def search_aggregate_shard(q_local, k_slab, v_slab, ff_slab, bf_slab, p: ShardPlan, cfg, ctx=None,
+                           check=True):
+    """Search + fused softmax + wpsum for the owned frames on the device (C-ABI frame-range
+    entry points).  q_local holds the owned frames only; Q's halo is never read."""
+    import torch
+
+    from . import snls as S
+
+    q_slab = q_local
+    if q_local.shape[0] != k_slab.shape[0]:
+        q_slab = torch.zeros_like(k_slab)
+        q_slab[p.t0:p.t1].copy_(q_local)
+    res = S.shifted_nls_forward(q_slab, k_slab, ff_slab, bf_slab, cfg, want_weights=True,
+                                frames=(p.t0, p.t1), ctx=ctx, check=check)
+    out, counts = S.wpsum(v_slab, res.weights, res.offsets, cfg, frames=(p.t0, p.t1), ctx=ctx,
+                          check=check)
+    return res, out, counts

@@ -111,6 +111,10 @@ def lib() -> C.CDLL:
             P = C.POINTER(_Config)
             L.snls_search_fwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, C.c_int,
                                           VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_search_fwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int, VOIDP, VOIDP,
+                                                 VOIDP, VOIDP, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
+            L.snls_wpsum_fwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int, VOIDP, VOIDP,
+                                                VOIDP, VOIDP, VOIDP]
             L.snls_search_grid.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_topl.argtypes = [VOIDP, C.c_int64, C.c_int, VOIDP, VOIDP, C.c_int, VOIDP, VOIDP]
             L.snls_replay.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP]
@@ -267,19 +271,22 @@ class SearchResult:
 
 def shifted_nls_forward(q, k, fflow, bflow, cfg: SearchConfig, mode: int = MODE_FUSED,
                         want_chains: bool = True, want_weights: bool = False,
-                        ctx: Optional[Context] = None, check: bool = True, out=None) -> SearchResult:
-    """snls::shifted_nls_forward (search.hpp:126-128). fflow/bflow None => nls_forward."""
+                        ctx: Optional[Context] = None, check: bool = True, out=None,
+                        frames=None) -> SearchResult:
+    """snls::shifted_nls_forward (search.hpp:126-128). fflow/bflow None => nls_forward.
+    `frames=(t0, t1)` searches only the query rows of frames [t0, t1) (frame sharding)."""
     import torch
 
     ctx = ctx or context(q.device.index)
     t, h, w, f = q.shape
+    t0, t1 = frames if frames is not None else (0, t)
     if tuple(k.shape) != tuple(q.shape):
         raise DomainError("search: query and key shapes differ")
     if fflow is not None and (tuple(fflow.shape) != (t, h, w, 2) or tuple(bflow.shape) != (t, h, w, 2)):
         raise DomainError("search: flow shape does not match the video")
     c = _cfg(cfg)
     _raise(lib().snls_validate_config(C.byref(c)))
-    rows = t * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    rows = (t1 - t0) * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
     if out is None:
         sims = torch.empty((rows, cfg.topl), device=q.device, dtype=torch.float32)
         offs = torch.empty((rows, cfg.topl, 3), device=q.device, dtype=torch.float32)
@@ -289,13 +296,13 @@ def shifted_nls_forward(q, k, fflow, bflow, cfg: SearchConfig, mode: int = MODE_
                    if want_weights else None)
     else:
         sims, offs, chains, weights = out
-    _raise(lib().snls_search_fwd(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(fflow),
-                                 _ptr(bflow), int(mode), _ptr(sims), _ptr(offs), _ptr(chains),
-                                 _ptr(weights)))
+    _raise(lib().snls_search_fwd_frames(ctx.h, C.byref(c), _dims(q), int(t0), int(t1), _ptr(q),
+                                        _ptr(k), _ptr(fflow), _ptr(bflow), int(mode), _ptr(sims),
+                                        _ptr(offs), _ptr(chains), _ptr(weights)))
     if check:
         ctx.sync_check()
     res = SearchResult(sims, offs, chains, weights, cfg)
-    res._grid = (t, (h - 1) // cfg.stride0 + 1, (w - 1) // cfg.stride0 + 1)
+    res._grid = (t1 - t0, (h - 1) // cfg.stride0 + 1, (w - 1) // cfg.stride0 + 1)
     return res
 
 
@@ -384,9 +391,10 @@ def softmax_rows(sims, beta: float, ctx=None, check=True):
     return w
 
 
-def _agg_shape_checks(v, weights, offsets, cfg):
+def _agg_shape_checks(v, weights, offsets, cfg, frames=None):
     t, h, w, f = v.shape
-    rows = t * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    t0, t1 = frames if frames is not None else (0, t)
+    rows = (t1 - t0) * ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
     validate(cfg)
     if not cfg.hole_free():
         raise ConfigError("aggregate: (ps-1)/2 < stride0 is required for hole-free output")
@@ -396,21 +404,23 @@ def _agg_shape_checks(v, weights, offsets, cfg):
         raise DomainError("aggregate: weight/offset L does not match the config")
 
 
-def wpsum(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True, out=None):
-    """snls::wpsum (aggregate.hpp:53-54) -> (video, counts)."""
+def wpsum(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True, out=None, frames=None):
+    """snls::wpsum (aggregate.hpp:53-54) -> (video, counts).  `frames=(t0, t1)` aggregates
+    only the output frames [t0, t1) from those frames' query rows (frame sharding)."""
     import torch
 
     ctx = ctx or context(v.device.index)
-    _agg_shape_checks(v, weights, offsets, cfg)
+    _agg_shape_checks(v, weights, offsets, cfg, frames)
     c = _cfg(cfg)
     t, h, w, f = v.shape
+    t0, t1 = frames if frames is not None else (0, t)
     if out is None:
-        o = torch.empty_like(v)
-        counts = torch.empty((t, h, w), device=v.device, dtype=torch.int32)
+        o = torch.empty((t1 - t0, h, w, f), device=v.device, dtype=torch.float32)
+        counts = torch.empty((t1 - t0, h, w), device=v.device, dtype=torch.int32)
     else:
         o, counts = out
-    _raise(lib().snls_wpsum_fwd(ctx.h, C.byref(c), _dims(v), _ptr(v), _ptr(weights), _ptr(offsets),
-                                _ptr(o), _ptr(counts)))
+    _raise(lib().snls_wpsum_fwd_frames(ctx.h, C.byref(c), _dims(v), int(t0), int(t1), _ptr(v),
+                                       _ptr(weights), _ptr(offsets), _ptr(o), _ptr(counts)))
     if check:
         ctx.sync_check()
     return o, counts

@@ -1,0 +1,110 @@
+"""CPU (gloo, world size 2 and 3): frame sharding with a wt-frame halo.
+
+Each rank owns a contiguous frame range, assembles its slab [a-wt, b+wt) ∩ [0, T) through
+paper_2309_16849_b200.shard.exchange (batched point-to-point send/recv -- NCCL on the GPU
+box, gloo here), and computes its rows on the slab.  With the oracle as the compute the
+sharded rows must equal the unsharded ones BIT FOR BIT: that pins the halo plan, the
+exchange and the frame-range semantics the CUDA entry points (snls_*_frames) implement."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2309_16849_b200 import shard
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_plan_partitions_and_transfers_pair_up():
+    for T in (5, 8, 13, 64):
+        for world in (1, 2, 3, 4, 8):
+            if world > T:
+                continue
+            for wt in (0, 1, 2, 3):
+                plans = [shard.plan(T, world, r, wt) for r in range(world)]
+                owned = sorted(f for p in plans for f in range(p.a, p.b))
+                assert owned == list(range(T))
+                for p in plans:
+                    assert p.lo == max(0, p.a - wt) and p.hi == min(T, p.b + wt)
+                    for peer, rng, kind in shard.transfers(p):
+                        other = {(q, r2, k2) for q, r2, k2 in shard.transfers(plans[peer])}
+                        assert (p.rank, rng, "send" if kind == "recv" else "recv") in other
+                    # the halo is exactly the slab minus the owned frames
+                    recv = sorted(f for _, (lo, hi), k in shard.transfers(p) if k == "recv"
+                                  for f in range(lo, hi))
+                    assert recv == [f for f in range(p.lo, p.hi) if not p.a <= f < p.b]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, T, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Cfg, Checker
+    from paper_2309_16849_b200 import shard as SH
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    P = Checker("port")
+    H = W = 10
+    F = 4
+    cfg = Cfg(ws=3, wt=2, ps=3, stride0=2, stride1=1.0, topl=3, metric="l2", softmax_scale=0.1)
+    # every rank can generate only its own frames (per-frame seeds)
+    def frame(t, seed, lo, hi, c):
+        return P.uniform(seed * 1000 + t, lo, hi, H * W * c).reshape(H, W, c)
+    p = SH.plan(T, world, rank, cfg.wt)
+    own_v = torch.tensor(np.stack([frame(t, 500, -1, 1, F) for t in range(p.a, p.b)]).astype(np.float32))
+    own_ff = torch.tensor(np.stack([frame(t, 501, -1.5, 1.5, 2) for t in range(p.a, p.b)]).astype(np.float32))
+    own_bf = torch.tensor(np.stack([frame(t, 502, -1.5, 1.5, 2) for t in range(p.a, p.b)]).astype(np.float32))
+    v = SH.exchange(own_v, p).double().numpy()
+    ff = SH.exchange(own_ff, p).double().numpy()
+    bf = SH.exchange(own_bf, p).double().numpy()
+    res = P.search_fwd(v, v, ff, bf, cfg)          # Q = K = V, slab as a clip
+    nq = ((H - 1) // cfg.stride0 + 1) * ((W - 1) // cfg.stride0 + 1)
+    rows = slice(p.t0 * nq, p.t1 * nq)
+    wts = P.softmax_rows(res["sims"], cfg.softmax_scale)
+    out, counts = P.wpsum(v, wts, res["offsets"], cfg)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), slab=v, sims=res["sims"][rows],
+             offsets=res["offsets"][rows], out=out[p.t0:p.t1], counts=counts[p.t0:p.t1],
+             a=p.a, b=p.b, lo=p.lo, hi=p.hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T", [(2, 7), (3, 8)])
+def test_gloo_halo_exchange_matches_unsharded_oracle(tmp_path, world, T):
+    import torch.multiprocessing as mp
+
+    from oracle.oracle import Cfg, Checker
+
+    mp.spawn(_worker, args=(world, _free_port(), T, str(tmp_path)), nprocs=world, join=True)
+    P = Checker("port")
+    H = W = 10
+    F = 4
+    cfg = Cfg(ws=3, wt=2, ps=3, stride0=2, stride1=1.0, topl=3, metric="l2", softmax_scale=0.1)
+
+    def frame(t, seed, lo, hi, c):
+        return P.uniform(seed * 1000 + t, lo, hi, H * W * c).reshape(H, W, c)
+    v = np.stack([frame(t, 500, -1, 1, F) for t in range(T)]).astype(np.float32).astype(np.float64)
+    ff = np.stack([frame(t, 501, -1.5, 1.5, 2) for t in range(T)]).astype(np.float32).astype(np.float64)
+    bf = np.stack([frame(t, 502, -1.5, 1.5, 2) for t in range(T)]).astype(np.float32).astype(np.float64)
+    full = P.search_fwd(v, v, ff, bf, cfg)
+    wts = P.softmax_rows(full["sims"], cfg.softmax_scale)
+    fout, fcounts = P.wpsum(v, wts, full["offsets"], cfg)
+    nq = 25
+    for r in range(world):
+        z = np.load(tmp_path / f"rank{r}.npz")
+        a, b, lo, hi = int(z["a"]), int(z["b"]), int(z["lo"]), int(z["hi"])
+        assert np.array_equal(z["slab"], v[lo:hi])                    # halo frames arrived intact
+        assert np.array_equal(z["sims"], full["sims"][a * nq:b * nq])   # bitwise, not approx
+        assert np.array_equal(z["offsets"], full["offsets"][a * nq:b * nq])
+        assert np.array_equal(z["out"], fout[a:b]) and np.array_equal(z["counts"], fcounts[a:b])

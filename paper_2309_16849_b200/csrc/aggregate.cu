@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
     const int x = x0 + p;
     if (x >= a.d.w) return;
     const AxisUnits uy = axis_units(y, a.d.stride0, a.ps / 2, (a.d.nh - 1) * a.d.stride0);
-    const size_t pix = (size_t(ti) * a.d.h + y) * a.d.w + x;
+    const size_t pix = (size_t(ti - a.d.t0) * a.d.h + y) * a.d.w + x;  // local output pixel
     if (!stack) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         const int cnt = gather_tiled<4>(a, s_desc, g, uy, y, x, 0, a.topl, c, acc);

@@ -220,6 +220,7 @@ def run_ours(args, wl):
         vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
     stream = torch.cuda.current_stream(dev)
     ctx = S.context(local)
+    ctx.set_search_kernel(args.search_kernel)
     L = wl["topl"]
     sims = torch.empty((rows, L), device=dev)
     offs = torch.empty((rows, L, 3), device=dev)
@@ -470,6 +471,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-crop", type=int, default=96)
+    ap.add_argument("--search-kernel", default=os.environ.get("SNLS_SEARCH_KERNEL", "auto"),
+                    choices=["auto", "tiled", "stream"], help="stride1 == 1 register plan")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]

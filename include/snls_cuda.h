@@ -85,10 +85,15 @@ int snls_ctx_set_stream(snls_ctx* ctx, void* cuda_stream);
 int snls_ctx_sync_check(snls_ctx* ctx);
 /* Number of kernels this context has launched (evidence for bench.py's gpu_launches). */
 int snls_ctx_launch_count(snls_ctx* ctx, int64_t* out);
-/* Kernel path the last search_fwd took: 0 generic per-slot, 1 tiled stride1 == 1. */
+/* Kernel path the last search_fwd took: 0 generic per-slot, 1 region-row tiled
+ * (stride1 == 1), 2 full grid, 3 query-stationary streaming (stride1 == 1). */
 int snls_ctx_last_search_path(snls_ctx* ctx, int* out);
 /* Force the generic per-slot search path (1) or allow the tiled one (0, default). */
 int snls_ctx_force_generic(snls_ctx* ctx, int on);
+/* stride1 == 1 register plan: 0 auto (streaming where instantiated, else tiled),
+ * 1 region-row tiled, 2 streaming.  Results agree to the parity tolerance; each plan is
+ * deterministic and tie-exact on its own. */
+int snls_ctx_set_search_kernel(snls_ctx* ctx, int kind);
 
 /* ---- device memory through the context (so C++ callers need no CUDA headers) --------- */
 int snls_device_alloc(snls_ctx* ctx, uint64_t bytes, void** out);

@@ -20,6 +20,7 @@ struct snls_ctx {
     int64_t launches = 0;
     int num_sms = 148;
     int force_generic = 0;
+    int search_kernel = 0;
     int last_path = -1;
 };
 
@@ -222,6 +223,13 @@ int snls_ctx_last_search_path(snls_ctx* ctx, int* out) {
     return SNLS_OK;
 }
 
+int snls_ctx_set_search_kernel(snls_ctx* ctx, int kind) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (kind < 0 || kind > 2) return fail(SNLS_EARG, "set_search_kernel: kind must be 0, 1 or 2");
+    ctx->search_kernel = kind;
+    return SNLS_OK;
+}
+
 int snls_ctx_force_generic(snls_ctx* ctx, int on) {
     if (int rc = check_ctx(ctx)) return rc;
     ctx->force_generic = on;
@@ -332,8 +340,8 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
         int produced = 0;
         if (!ctx->force_generic && cfg->stride1 == 1.0) {
             TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
-                           sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid};
-            produced = launch_search_tiled(ts, ctx->stream);
+                           sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid, ctx->search_kernel};
+            produced = launch_search_tiled(ts, ctx->stream, nullptr);
             if (produced < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
         }
         if (produced == 0) {
@@ -353,16 +361,16 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
         return after_launch(ctx, launched + produced + 1, "snls_search_fwd(fullgrid)");
     }
 
-    int tiled = 0;
+    int tiled = 0, used = 0;
     if (!ctx->force_generic && cfg->stride1 == 1.0) {
         TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
-                       sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr};
-        tiled = launch_search_tiled(ts, ctx->stream);
+                       sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr, ctx->search_kernel};
+        tiled = launch_search_tiled(ts, ctx->stream, &used);
         if (tiled < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
     }
     if (tiled > 0) {
         launched += tiled;
-        ctx->last_path = 1;
+        ctx->last_path = used == 2 ? 3 : 1;
     } else {
         GenericSearch gs{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric,
                          cfg->stride1, beta, sims, offsets, chains, weights, nullptr, nullptr, 1, ctx->err,

@@ -32,6 +32,7 @@ struct TiledSearch {
     int* err;
     int num_sms;
     float* grid;  // kFullGrid: write every window score (rows x slots) and skip selection
+    int kernel;   // register plan: 0 auto, 1 region-row tiled, 2 streaming
 };
 
 struct AggArgs {
@@ -46,7 +47,10 @@ struct AggArgs {
 int launch_flows_check(const float* ff, const float* bf, int64_t n, int* err, cudaStream_t st);
 int launch_search_generic(const GenericSearch& g, cudaStream_t st);
 // Returns 0 when (ws, ps, f, topl) has no tiled instantiation (caller falls back).
-int launch_search_tiled(const TiledSearch& s, cudaStream_t st);
+// `used` (optional) receives the plan that ran: 1 tiled, 2 streaming.
+int launch_search_tiled(const TiledSearch& s, cudaStream_t st, int* used);
+// Query-stationary streaming variant (search_stream.cu); 0 when not instantiated.
+int launch_search_stream(const TiledSearch& s, cudaStream_t st);
 int launch_topl(int64_t rows, int cols, const float* full, const float* full_offsets, int topl,
                 float* sel, float* sel_offsets, int* err, cudaStream_t st);
 int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,

@@ -1,0 +1,380 @@
+// Query-stationary streaming Shifted-NLS forward for stride1 == 1: fused search + streaming
+// top-L (+ optional softmax epilogue), sm_100a, FP32 FMA pipe.
+//
+// Same contract and tie rules as search_tiled.cu; different register plan, built for large
+// patches (ps = 7 spills the tiled kernel's interpolated-row cache) and for cutting the
+// per-region-row query reloads:
+//  * G = F / VEC lanes per query, lane gl owns channels [gl*VEC, gl*VEC+VEC).  The whole
+//    ps x ps query patch of the lane's channels is loaded ONCE into registers and reused for
+//    every frame, region row and slot (search.cpp:129-132 reads it per slot).
+//  * Per (query, frame) the (ws+ps-1)^2 key region is interpolated exactly once, streamed
+//    pixel by pixel: region pixel (r, j) is blended from the two raw rows r, r+1 (sliding
+//    column window, so 2 loads per pixel) and immediately contributes to every slot that
+//    reads it, acc[s][j - px] += m(Q[P-1-s][px], k) -- nothing is cached per region row.
+//  * Slot rows rotate through acc[P][W] as in the tiled kernel; a slot row completes after
+//    its last region row, is reduce-scattered over the G lanes (identical addition tree for
+//    every slot, so duplicate candidates tie exactly) and streamed into a rank-sharded
+//    register top-L with strict '>' in ascending slot order (topl_insert, search.cpp:187-197).
+//    Candidates not above the current rank topl-1 can never be selected and stop at one
+//    compare.
+// Per slot the accumulation order is (py, px, channel) ascending within a lane, then the
+// fixed butterfly over lanes -- the same for every slot of every frame.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace snls_gpu {
+
+namespace {
+
+constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const float* p, float (&o)[VEC]) {
+    if constexpr (VEC == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else if constexpr (VEC == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = v.x; o[1] = v.y;
+    } else {
+        o[0] = __ldg(p);
+    }
+}
+
+template <int P, int W, int VEC, int G, int KMAX>
+struct StreamCfg {
+    static constexpr int HP = P / 2, HW = W / 2, R = W + P - 1, F = G * VEC;
+    static constexpr int QPW = 32 / G, WARPS = 4, QPB = QPW * WARPS;
+    static constexpr int M = KMAX / G > 0 ? KMAX / G : 1;  // list ranks per lane
+    // reduce-scatter geometry: W slots padded to NPAD; if NPAD >= G every lane ends with
+    // NPL consecutive slots, else 2^SH neighbouring lanes share one slot (all-reduced)
+    static constexpr int NPAD = pow2ceil(W);
+    static constexpr int NPL = NPAD >= G ? NPAD / G : 1;
+    static constexpr int SH = NPAD >= G ? 0 : ilog2(G / NPAD);
+};
+
+// Rank-sharded group list (see search_tiled.cu group_insert): lane gl holds ranks
+// [gl*M, gl*M+M) sorted descending; strict '>' keeps earlier slots ahead on ties.
+template <int G, int M>
+__device__ __forceinline__ void list_insert(float (&ev)[M], uint32_t (&es)[M], float v, uint32_t s,
+                                            int gl) {
+    float pv = __shfl_up_sync(0xffffffffu, ev[M - 1], 1, G);
+    uint32_t ps = __shfl_up_sync(0xffffffffu, es[M - 1], 1, G);
+    if (gl == 0) pv = INFINITY;
+    float nv[M];
+    uint32_t ns[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const float above = j == 0 ? pv : ev[j - 1];
+        const uint32_t above_s = j == 0 ? ps : es[j - 1];
+        const bool ga = v > above, gc = v > ev[j];
+        nv[j] = ga ? above : (gc ? v : ev[j]);
+        ns[j] = ga ? above_s : (gc ? s : es[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        ev[j] = nv[j];
+        es[j] = ns[j];
+    }
+}
+
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB>
+__global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a) {
+    static_assert(W >= P, "window narrower than the patch: not instantiated");
+    using C = StreamCfg<P, W, VEC, G, KMAX>;
+    constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F, M = C::M;
+    __shared__ uint64_t s_keys[C::QPB][16];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane / G, gl = lane % G;
+    const int qslot = warp * C::QPW + gq;
+    const int64_t row_raw = int64_t(blockIdx.x) * C::QPB + qslot;
+    const bool row_ok = row_raw < a.d.rows;
+    const int64_t row = row_ok ? row_raw : a.d.rows - 1;
+    int qt, qy, qx;
+    row_coords(a.d, row, qt, qy, qx);
+    const int H = a.d.h, Wd = a.d.w;
+    const unsigned rowF = unsigned(Wd) * F;  // floats per image row
+    const size_t frame_elems = size_t(H) * rowF;
+    const int c0 = gl * VEC;
+    const int nfr = 2 * a.wt + 1;
+
+    // ---- the query patch, reflected integer pixels (search.cpp:129-132), in registers
+    float qv[P][P][VEC];
+    {
+        const float* qb = a.q + size_t(qt) * frame_elems + c0;
+#pragma unroll
+        for (int py = 0; py < P; ++py) {
+            const float* qr = qb + size_t(reflect_near(qy + py - HP, H)) * rowF;
+#pragma unroll
+            for (int px = 0; px < P; ++px) ldv<VEC>(qr + size_t(reflect_near(qx + px - HP, Wd)) * F, qv[py][px]);
+        }
+    }
+
+    float ev[M];
+    uint32_t es[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        ev[j] = -INFINITY;
+        es[j] = 0xffffffffu;
+    }
+    // rank topl-1 of the group list is the selection threshold
+    const int thr_lane = (lane / G) * G + (a.topl - 1) / M, thr_idx = (a.topl - 1) % M;
+
+    for (int fp = 0; fp < nfr; ++fp) {
+        const int dt = scan_dt(fp), kt = qt + dt;
+        const bool on = row_ok && kt >= 0 && kt < a.d.t;
+        if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
+            if (a.grid && row_ok) {
+                float* g = a.grid + size_t(row) * nfr * W * W + size_t(fp) * W * W;
+                for (int s = gl; s < W * W; s += G) g[s] = -INFINITY;
+            }
+            continue;
+        }
+        double sdy = 0.0, sdx = 0.0;
+        if (on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
+        const double cy = double(qy) + sdy, cx = double(qx) + sdx;
+        const double fby = floor(cy), fbx = floor(cx);
+        const float fy = float(cy - fby), fx = float(cx - fbx);
+        const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+        const float w10 = fy * (1.f - fx), w11 = fy * fx;
+        const int by = int(fby) - HW - HP, bx = int(fbx) - HW - HP;
+        const float* kb = a.k + size_t(on ? kt : qt) * frame_elems + c0;
+        // reflected column offsets of the region (tensor.cpp:23-29), once per frame
+        unsigned xo[R + 1];
+#pragma unroll
+        for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * F;
+
+        float acc[P][W];
+#pragma unroll
+        for (int s = 0; s < P; ++s)
+#pragma unroll
+            for (int b = 0; b < W; ++b) acc[s][b] = 0.f;
+
+        const uint32_t slot_base = uint32_t(fp) * W * W;
+
+        // One region row: stream its R pixels through all P rotating slot rows.  On the
+        // first/last P-1 region rows some of those slot rows lie outside the window; their
+        // accumulators are updated anyway (they are never emitted: a slot row is emitted
+        // only after its last region row) -- a uniform straight-line body with no guards
+        // beats guarded bodies on this pipe (measured: per-row compile-time ranges cost
+        // more in instruction-cache misses than the wasted FMAs).
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+            const float* p0 = kb + unsigned(reflect_near(by + r, H)) * rowF;
+            const float* p1 = kb + unsigned(reflect_near(by + r + 1, H)) * rowF;
+            float a0[VEC], a1[VEC];
+            ldv<VEC>(p0 + xo[0], a0);
+            ldv<VEC>(p1 + xo[0], a1);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                float b0[VEC], b1[VEC];
+                ldv<VEC>(p0 + xo[j + 1], b0);
+                ldv<VEC>(p1 + xo[j + 1], b1);
+                float kr[VEC];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    kr[v] = fmaf(w11, b1[v], fmaf(w10, a1[v], fmaf(w01, b0[v], w00 * a0[v])));
+                    a0[v] = b0[v];
+                    a1[v] = b1[v];
+                }
+#pragma unroll
+                for (int s = 0; s < P; ++s) {
+#pragma unroll
+                    for (int px = 0; px < P; ++px) {
+                        const int b = j - px;
+                        if (b < 0 || b >= W) continue;  // compile time
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            if (METRIC == SNLS_METRIC_IP) {
+                                acc[s][b] = fmaf(qv[P - 1 - s][px][v], kr[v], acc[s][b]);
+                            } else {
+                                const float d = qv[P - 1 - s][px][v] - kr[v];
+                                acc[s][b] = fmaf(d, d, acc[s][b]);
+                            }
+                        }
+                    }
+                }
+            }
+
+            // ---- slot row r-(P-1) complete: reduce-scatter over the G lanes, then stream
+            if (r >= P - 1) {
+                float v[C::NPAD];
+#pragma unroll
+                for (int b = 0; b < C::NPAD; ++b) v[b] = b < W ? acc[0][b] : 0.f;
+                // scatter levels: the lane bit for m picks the upper half of the values
+#pragma unroll
+                for (int lev = 0; lev < ilog2(G); ++lev) {
+                    const int m = G >> (lev + 1), n = C::NPAD >> lev;  // n values before
+                    if (n > 1) {
+                        const bool hi = (gl & m) != 0;
+#pragma unroll
+                        for (int i = 0; i < n / 2; ++i) {
+                            const float keep = hi ? v[i + n / 2] : v[i];
+                            const float send = hi ? v[i] : v[i + n / 2];
+                            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                        }
+                    } else {  // more lanes than slots: all-reduce the remaining levels
+                        v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+                    }
+                }
+                const int arow = r - (P - 1);
+                // lane gl holds slots (gl >> SH) * NPL + i, i < NPL; owner lanes have the
+                // low SH bits clear
+                const int sb = (gl >> C::SH) * C::NPL;
+                const bool owner = (gl & ((1 << C::SH) - 1)) == 0;
+                if (a.grid) {  // kFullGrid: materialise the scores (-inf off-clip), no selection
+#pragma unroll
+                    for (int i = 0; i < C::NPL; ++i) {
+                        const int b = sb + i;
+                        const float val = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
+                        if (row_ok && owner && b < W)
+                            a.grid[size_t(row) * nfr * W * W + slot_base + arow * W + b] = on ? val : -INFINITY;
+                    }
+                } else {
+                    float thr = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < M; ++j) thr = j == thr_idx ? ev[j] : thr;
+                    thr = __shfl_sync(0xffffffffu, thr, thr_lane);
+                    uint32_t pend = 0;
+#pragma unroll
+                    for (int i = 0; i < C::NPL; ++i) {
+                        const int b = sb + i;
+                        v[i] = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
+                        if (on && owner && b < W && v[i] > thr) pend |= 1u << i;
+                    }
+                    // survivors one at a time, lanes then slots ascending (= slot order)
+                    while (__any_sync(0xffffffffu, pend != 0)) {
+                        const unsigned want = __ballot_sync(0xffffffffu, pend != 0);
+                        const unsigned gmask =
+                            (want >> (gq * G)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
+                        const int src = gmask ? gq * G + (__ffs(gmask) - 1) : lane;
+                        const int isrc = pend ? (__ffs(pend) - 1) : 0;
+                        float cv = -INFINITY;
+#pragma unroll
+                        for (int i = 0; i < C::NPL; ++i) cv = (i == isrc) ? v[i] : cv;
+                        const uint32_t cs = slot_base + uint32_t(arow * W + sb + isrc);
+                        float bv = __shfl_sync(0xffffffffu, cv, src);
+                        const uint32_t bs = __shfl_sync(0xffffffffu, cs, src);
+                        if (!gmask) bv = -INFINITY;  // keeps the shuffles warp-uniform
+                        list_insert<G, M>(ev, es, bv, bs, gl);
+                        if (lane == src && gmask) pend &= pend - 1;
+                    }
+                }
+            }
+            // rotate: acc[s] tracks slot row r-(P-1)+s
+#pragma unroll
+            for (int s = 0; s + 1 < P; ++s)
+#pragma unroll
+                for (int b = 0; b < W; ++b) acc[s][b] = acc[s + 1][b];
+#pragma unroll
+            for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
+        }
+    }
+
+    if (a.grid) return;  // selection happens in the top_l pass over the grid
+
+    // ---- lane gl owns ranks gl*M .. gl*M+M-1 of the merged list
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const int li = gl * M + j;
+        if (li < a.topl) s_keys[qslot][li] = eligible(ev[j]) ? pack_key(ev[j], es[j]) : 0ull;
+    }
+    __syncwarp();
+
+    // ---- emit_row (search.cpp:207-234) + softmax epilogue (aggregate.cpp:16-37)
+    float zmax = -INFINITY;
+    for (int li = gl; row_ok && li < a.topl; li += G) {
+        const uint64_t key = s_keys[qslot][li];
+        const size_t e = size_t(row) * a.topl + li;
+        float v = -INFINITY, o1 = 0.f, o2 = 0.f;
+        int dt = 0;
+        if (key != 0ull) {
+            const uint32_t slot = key_slot(key);
+            v = key_value(key);
+            const int fp = int(slot) / (W * W), rem = int(slot) % (W * W);
+            dt = scan_dt(fp);
+            double sdy, sdx;
+            shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
+            const double ky = (double(qy) + sdy) + double(rem / W - HW);
+            const double kx = (double(qx) + sdx) + double(rem % W - HW);
+            o1 = float(ky - double(qy));
+            o2 = float(kx - double(qx));
+        }
+        a.sims[e] = v;
+        a.offsets[e * 3 + 0] = float(dt);
+        a.offsets[e * 3 + 1] = o1;
+        a.offsets[e * 3 + 2] = o2;
+        if (a.chains && a.wt > 1) {
+            const int cs = a.wt - 1;
+            float* lk = a.chains + e * size_t(cs) * 6;
+            for (int j = 0; j < cs * 6; ++j) lk[j] = 0.f;
+            if (dt > 1 || dt < -1) {
+                double sdy, sdx;
+                shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, lk);
+            }
+        }
+        zmax = fmaxf(zmax, a.beta * v);
+    }
+    if (a.weights) {
+#pragma unroll
+        for (int m = G / 2; m >= 1; m >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, m));
+        float sum = 0.f;
+        for (int li = gl; row_ok && li < a.topl; li += G) {
+            const float z = a.beta * key_value(s_keys[qslot][li]);
+            if (!isfinite(z)) latch(a.err, kErrSoftmax);
+            sum += __expf(z - zmax);
+        }
+#pragma unroll
+        for (int m = G / 2; m >= 1; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+        for (int li = gl; row_ok && li < a.topl; li += G) {
+            const size_t e = size_t(row) * a.topl + li;
+            a.weights[e] = __expf(a.beta * key_value(s_keys[qslot][li]) - zmax) / sum;
+        }
+    }
+}
+
+template <int P, int W, int VEC, int G, int MINB>
+int launch_one(const TiledSearch& s, cudaStream_t st) {
+    using C = StreamCfg<P, W, VEC, G, 16>;
+    const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
+    if (s.metric == SNLS_METRIC_IP)
+        search_stream_kernel<P, W, VEC, G, 16, SNLS_METRIC_IP, MINB><<<blocks, 128, 0, st>>>(s);
+    else
+        search_stream_kernel<P, W, VEC, G, 16, SNLS_METRIC_L2, MINB><<<blocks, 128, 0, st>>>(s);
+    return 1;
+}
+
+// Channel split per (ps, F): VEC channels per lane, G = F / VEC lanes per query.  Large
+// patches take VEC = 2 so the ps^2 query patch fits the register file next to the ps x ws
+// accumulators.
+template <int P, int W>
+int launch_by_f(const TiledSearch& s, cudaStream_t st) {
+    if constexpr (P >= 5) {
+        switch (s.d.f) {
+            case 64: return launch_one<P, W, 2, 32, 2>(s, st);
+            default: return 0;
+        }
+    } else {
+        switch (s.d.f) {
+            case 32: return launch_one<P, W, 4, 8, 3>(s, st);
+            case 64: return launch_one<P, W, 4, 16, 3>(s, st);
+            default: return 0;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_search_stream(const TiledSearch& s, cudaStream_t st) {
+    if (s.topl > 16) return 0;
+    if (s.ps == 7 && s.ws == 9) return launch_by_f<7, 9>(s, st);   // c2 / c3
+    if (s.ps == 3 && s.ws == 11) return launch_by_f<3, 11>(s, st); // c4
+    if (s.ps == 3 && s.ws == 9) return launch_by_f<3, 9>(s, st);   // c5
+    return 0;
+}
+
+}  // namespace snls_gpu

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
 inline int tiled_minb() {
     static const int v = [] {
         const char* e = std::getenv("SNLS_TILED_MINB");
-        return (e && std::atoi(e) == 4) ? 4 : 3;
+        return (e && std::atoi(e) == 4) ? 4 : ((e && std::atoi(e) == 2) ? 2 : 3);
     }();
     return v;
 }
@@ -377,7 +377,10 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
 
 template <int P, int W, int VEC, int G, int KMAX>
 int launch_cfg(const TiledSearch& s, cudaStream_t st) {
-    if (P == 3 && G == 8 && tiled_minb() == 4) return launch_cfg_b<P, W, VEC, G, KMAX, 4>(s, st);
+    if constexpr (P == 3 && G == 8)
+        if (tiled_minb() == 4) return launch_cfg_b<P, W, VEC, G, KMAX, 4>(s, st);
+    if constexpr (P == 7)  // the ps = 7 plan spills under the 168-register cap
+        return launch_cfg_b<P, W, VEC, G, KMAX, 2>(s, st);
     return launch_cfg_b<P, W, VEC, G, KMAX, 3>(s, st);
 }
 
@@ -402,7 +405,16 @@ int launch_by_k(const TiledSearch& s, cudaStream_t st) {
 }  // namespace
 
 // Instantiated (ps, ws) pairs; anything else takes the generic path.
-int launch_search_tiled(const TiledSearch& s, cudaStream_t st) {
+int launch_search_tiled(const TiledSearch& s, cudaStream_t st, int* used) {
+    // auto: the streaming plan for large patches (the tiled plan spills at ps = 7), the
+    // region-row tiled plan otherwise (faster at ps = 3 on B200, profiles/)
+    if (s.kernel == 2 || (s.kernel == 0 && s.ps >= 5)) {
+        if (int n = launch_search_stream(s, st)) {
+            if (used) *used = 2;
+            return n;
+        }
+    }
+    if (used) *used = 1;
     if (s.ps == 3 && s.ws == 11) return launch_by_k<3, 11>(s, st);  // c4
     if (s.ps == 3 && s.ws == 9) return launch_by_k<3, 9>(s, st);    // c5
     if (s.ps == 7 && s.ws == 9) return launch_by_k<7, 9>(s, st);    // c2 / c3

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
             L.snls_ctx_launch_count.argtypes = [VOIDP, C.POINTER(C.c_int64)]
             L.snls_ctx_last_search_path.argtypes = [VOIDP, C.POINTER(C.c_int)]
             L.snls_ctx_force_generic.argtypes = [VOIDP, C.c_int]
+            L.snls_ctx_set_search_kernel.argtypes = [VOIDP, C.c_int]
             L.snls_validate_config.argtypes = [C.POINTER(_Config)]
             P = C.POINTER(_Config)
             L.snls_search_fwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, C.c_int,
@@ -208,6 +209,10 @@ class Context:
 
     def force_generic(self, on: bool):
         _raise(lib().snls_ctx_force_generic(self.h, int(on)))
+
+    def set_search_kernel(self, kind: str):
+        """'auto' | 'tiled' | 'stream' register plan for the stride1 == 1 search."""
+        _raise(lib().snls_ctx_set_search_kernel(self.h, {"auto": 0, "tiled": 1, "stream": 2}[kind]))
 
 
 _ctxs: dict = {}

@@ -1,0 +1,63 @@
+"""GPU parity of every production register plan (the kernels the bench runs) at the BASELINE
+configs' ws / ps / wt / F / metric, on frames small enough for the oracle and with borders
+in play: the region-row tiled plan and the query-stationary streaming plan must each match
+the oracle (search_fwd + fused softmax), and each plan's full-grid mode must equal its fused
+mode bit for bit (test_search.cpp:317-347)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Cfg
+from tests.gpu_util import compare_search, dev, host, scfg, snls_mod
+from tests.helpers import REL_TOL, flow, max_rel, video
+
+pytestmark = pytest.mark.gpu
+
+# (name, T, H, W, F, cfg) -- BASELINE configs[1], [3], [4] shapes with reduced frames
+SHAPES = [
+    ("c2", 5, 30, 28, 64, Cfg(ws=9, wt=2, ps=7, stride0=4, topl=10, metric="ip",
+                              softmax_scale=1.0 / 3136)),
+    ("c4", 6, 34, 30, 32, Cfg(ws=11, wt=3, ps=3, stride0=2, topl=16, metric="l2",
+                              softmax_scale=1.0 / 288)),
+    ("c5", 5, 28, 34, 64, Cfg(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2",
+                              softmax_scale=1.0 / 576)),
+]
+
+_cache = {}
+
+
+def case(port, name, t, h, w, f, cfg):
+    if name not in _cache:
+        seed = {"c2": 11, "c4": 100, "c5": 500}[name]
+        q = video(port, t, h, w, f, seed)
+        k = q if name != "c2" else video(port, t, h, w, f, seed + 1)
+        ff, bf = flow(port, t, h, w, seed + 3, 2.0), flow(port, t, h, w, seed + 4, 2.0)
+        ref = port.search_fwd(q, k, ff, bf, cfg)
+        lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
+        wts = port.softmax_rows(ref["sims"], cfg.softmax_scale)
+        _cache[name] = (q, k, ff, bf, ref, lp1, wts)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("kernel,path", [("tiled", 1), ("stream", 3)])
+@pytest.mark.parametrize("name,t,h,w,f,cfg", SHAPES, ids=[s[0] for s in SHAPES])
+def test_register_plan_vs_oracle(port, kernel, path, name, t, h, w, f, cfg):
+    S = snls_mod()
+    q, k, ff, bf, ref, lp1, wts = case(port, name, t, h, w, f, cfg)
+    ctx = S.context()
+    ctx.set_search_kernel(kernel)
+    try:
+        args = (dev(q), dev(k), dev(ff), dev(bf), scfg(cfg))
+        r = S.shifted_nls_forward(*args, want_weights=True, ctx=ctx)
+        assert ctx.last_search_path() == path
+        excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
+        # near-tie rows (gradcheck_util.hpp:61-69) are common with k = 16 of 847 candidates
+        assert excluded < 0.5 * ref["sims"].shape[0]
+        assert max_rel(host(r.weights), wts) <= REL_TOL
+        g = S.shifted_nls_forward(*args, mode=1, want_weights=True, ctx=ctx)
+        for x, y in ((r.sims, g.sims), (r.offsets, g.offsets), (r.weights, g.weights)):
+            assert np.array_equal(host(x), host(y)), "full grid != fused for this plan"
+        again = S.shifted_nls_forward(*args, want_weights=True, ctx=ctx)
+        assert np.array_equal(host(again.sims), host(r.sims))
+        assert np.array_equal(host(again.offsets), host(r.offsets))
+    finally:
+        ctx.set_search_kernel("auto")

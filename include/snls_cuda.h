@@ -81,6 +81,7 @@ int snls_uniform_fill_f32(uint64_t seed, double lo, double hi, int64_t n, float*
 int snls_ctx_create(int device, void* cuda_stream, snls_ctx** out);
 int snls_ctx_destroy(snls_ctx* ctx);
 int snls_ctx_set_stream(snls_ctx* ctx, void* cuda_stream);
+int snls_ctx_get_stream(snls_ctx* ctx, void** cuda_stream);
 /* Synchronise the stream; report (and clear) latched device-side domain errors. */
 int snls_ctx_sync_check(snls_ctx* ctx);
 /* Number of kernels this context has launched (evidence for bench.py's gpu_launches). */
@@ -171,6 +172,31 @@ int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
 int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                    const float* grad_out, const int32_t* counts, const float* v,
                    const float* weights, const float* offsets, float* dv, float* dweights);
+
+/* ---- host-buffer pipeline (the search -> softmax_rows -> wpsum core of align_frames /
+ * run_benchmark, harness.cpp:105-154, 242-283, over HOST memory) ---------------------
+ * One call copies the clip in frame by frame on a copy stream, runs search (+ fused
+ * softmax) and wpsum per chunk of query frames on two compute streams as soon as the
+ * frames each chunk can reach have landed (qt + dt, |dt| <= wt), and copies each chunk's
+ * results back on a result stream: transfers overlap the kernels.  Synchronous: returns
+ * when all results are in host memory and the device error latch has been checked (domain
+ * errors as snls_ctx_sync_check).  The whole call is ordered after, and joined back into,
+ * the context's stream. */
+typedef struct snls_pipeline snls_pipeline;
+/* Pin / unpin caller memory (cudaHostRegister) so the pipeline's copies run asynchronously. */
+int snls_host_register(void* host_ptr, uint64_t bytes);
+int snls_host_unregister(void* host_ptr);
+/* Device buffers for a clip of `dims` under `cfg`; chunk_frames query frames per chunk. */
+int snls_pipeline_create(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int chunk_frames,
+                         snls_pipeline** out);
+int snls_pipeline_destroy(snls_pipeline* p);
+/* q, k, v HOST T x H x W x F (k and v may alias q: each distinct buffer is copied once);
+ * fflow, bflow HOST T x H x W x 2, or both NULL (nls_forward).  Outputs HOST, each may be
+ * NULL to skip it: sims rows x L, offsets rows x L x 3, weights rows x L, out T x H x W x F,
+ * counts T x H x W. */
+int snls_pipeline_run(snls_pipeline* p, const float* q, const float* k, const float* v,
+                      const float* fflow, const float* bflow, float* sims, float* offsets,
+                      float* weights, float* out, int32_t* counts);
 
 #ifdef __cplusplus
 }

@@ -24,14 +24,22 @@ struct snls_ctx {
     int last_path = -1;
 };
 
-namespace {
+namespace snls_capi {
 
 thread_local std::string g_err;
 
+// Record the message of a failure for snls_last_error() (also used by pipeline.cu).
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+}  // namespace snls_capi
+
+using snls_capi::fail;
+using snls_capi::g_err;
+
+namespace {
 
 int cuda_fail(cudaError_t e, const char* where) {
     return fail(SNLS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -208,6 +216,12 @@ int snls_ctx_destroy(snls_ctx* ctx) {
 int snls_ctx_set_stream(snls_ctx* ctx, void* stream) {
     if (int rc = check_ctx(ctx)) return rc;
     ctx->stream = static_cast<cudaStream_t>(stream);
+    return SNLS_OK;
+}
+
+int snls_ctx_get_stream(snls_ctx* ctx, void** out) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (out) *out = static_cast<void*>(ctx->stream);
     return SNLS_OK;
 }
 

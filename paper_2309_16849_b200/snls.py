@@ -126,6 +126,12 @@ def lib() -> C.CDLL:
             L.snls_gather_stack.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_wpsum_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
                                          VOIDP, VOIDP]
+            L.snls_ctx_get_stream.argtypes = [VOIDP, C.POINTER(VOIDP)]
+            L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
+            L.snls_host_unregister.argtypes = [VOIDP]
+            L.snls_pipeline_create.argtypes = [VOIDP, P, _Dims, C.c_int, C.POINTER(VOIDP)]
+            L.snls_pipeline_destroy.argtypes = [VOIDP]
+            L.snls_pipeline_run.argtypes = [VOIDP] + [VOIDP] * 10
             _lib = L
         return _lib
 
@@ -461,3 +467,57 @@ def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx
     if check:
         ctx.sync_check()
     return dv, dw
+
+
+# ---------------------------------------------------------------------------------------
+class Pipeline:
+    """Host-buffer search + fused softmax + wpsum over a clip (snls_pipeline_*, see
+    include/snls_cuda.h): frame-chunked kernels overlapped with the H2D input and D2H result
+    copies.  Arguments of run() are HOST tensors/arrays (torch CPU tensors -- pinned for
+    overlap -- or numpy arrays); q, k, v may be the same buffer (copied once)."""
+
+    def __init__(self, cfg: SearchConfig, dims, chunk_frames: int = 1, ctx: Optional[Context] = None):
+        self.ctx = ctx or context()
+        self.cfg = cfg
+        self.dims = tuple(int(x) for x in dims)
+        self._c = _cfg(cfg)
+        h = VOIDP()
+        _raise(lib().snls_pipeline_create(self.ctx.h, C.byref(self._c), _Dims(*self.dims),
+                                          int(chunk_frames), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def _hp(x):
+        if x is None:
+            return None
+        if hasattr(x, "data_ptr"):
+            if x.is_cuda or not x.is_contiguous():
+                raise SnlsError("snls pipeline: host buffers must be contiguous CPU tensors")
+            return VOIDP(x.data_ptr())
+        if not x.flags["C_CONTIGUOUS"]:
+            raise SnlsError("snls pipeline: host buffers must be C-contiguous")
+        return VOIDP(x.ctypes.data)
+
+    def run(self, q, k, v, fflow, bflow, sims=None, offsets=None, weights=None, out=None,
+            counts=None):
+        hp = self._hp
+        _raise(lib().snls_pipeline_run(self.h, hp(q), hp(k), hp(v), hp(fflow), hp(bflow),
+                                       hp(sims), hp(offsets), hp(weights), hp(out), hp(counts)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().snls_pipeline_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def host_register(buf) -> None:
+    """Pin a host numpy array / CPU tensor in place (cudaHostRegister)."""
+    ptr = buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data
+    n = buf.numel() * buf.element_size() if hasattr(buf, "numel") else buf.nbytes
+    _raise(lib().snls_host_register(VOIDP(ptr), n))

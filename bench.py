@@ -42,6 +42,12 @@ WORKLOADS = {
     "c2": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
                beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0,
                name="c2: 5x128x128x64, ws9 wt2 ps7 k10 ip s0=4"),
+    # BASELINE configs[2]: c2 shapes fwd + bwd (vid & flow grads); upstream gradients
+    # U[-1,1) seeds 16 (sims) and 17 (wpsum output)
+    "c3": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
+               beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0, train=True,
+               gs_seed=16, go_seed=17,
+               name="c3: 5x128x128x64, ws9 wt2 ps7 k10 ip s0=4, fwd + bwd (dQ dK dV dW dFlow)"),
     # BASELINE configs[4]: single video T=64 C=64 H=W=512 ws=9 wt=2 ps=3 k=10, frame-sharded
     # across ranks with a wt-frame NCCL halo (per-frame seeds 500*1000+t)
     "c5": dict(T=64, H=512, W=512, C=64, ws=9, wt=2, ps=3, topl=10, metric="l2", stride0=2,
@@ -228,18 +234,30 @@ def run_ours(args, wl):
     out = torch.empty_like(own_vid)
     counts = torch.empty(own_vid.shape[:3], device=dev, dtype=torch.int32)
     flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
+    train = wl.get("train", False)
+    if train:  # the tape's chains and the two upstream gradients
+        chains = torch.empty((rows, L, cfg.chain_stride(), 6), device=dev) if cfg.wt > 1 else None
+        g_sims = torch.from_numpy(S.uniform_fill(wl["gs_seed"], -1, 1, rows * L).reshape(rows, L)).to(dev)
+        g_out = torch.from_numpy(S.uniform_fill(wl["go_seed"], -1, 1, own_vid.numel())
+                                 .reshape(own_vid.shape)).to(dev)
+    bwd_ms = []
 
     def step():
         nonlocal vid, ff, bf
         if sharded and world > 1:  # the data path's only communication: the wt-frame halo
             vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
-        S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
-                              out=(sims, offs, None, wts), frames=frames)
+        res = S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
+                                    out=(sims, offs, chains if train else None, wts), frames=frames)
         ev_mid.record(stream)
         S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
+        if train:  # backward: wpsum_backward (dV, dW) then shifted_nls_backward (dQ, dK, dFlow)
+            ev_bwd.record(stream)
+            S.wpsum_backward(g_out, counts, vid, wts, offs, cfg, ctx=ctx, check=False)
+            S.shifted_nls_backward(g_sims, res, vid, vid, ctx=ctx, check=False)
 
     # correctness gate before timing: device error latch must be clean
     ev_mid = torch.cuda.Event(enable_timing=True)
+    ev_bwd = torch.cuda.Event(enable_timing=True)
     step()
     ctx.sync_check()
     for _ in range(args.warmup):
@@ -258,11 +276,12 @@ def run_ours(args, wl):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         ev_mid = torch.cuda.Event(enable_timing=True)
+        ev_bwd = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step()
         e2.record(stream)
-        evs.append((e0, ev_mid, e2))
+        evs.append((e0, ev_mid, e2, ev_bwd))
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     if world > 1:
@@ -271,9 +290,10 @@ def run_ours(args, wl):
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
     ctx.sync_check()
-    step_ms = [a.elapsed_time(c) for a, _, c in evs]
-    search_ms = [a.elapsed_time(b) for a, b, _ in evs]
-    wpsum_ms = [b.elapsed_time(c) for _, b, c in evs]
+    step_ms = [a.elapsed_time(c) for a, _, c, _ in evs]
+    search_ms = [a.elapsed_time(b) for a, b, _, _ in evs]
+    wpsum_ms = [b.elapsed_time(bw if train else c) for _, b, c, bw in evs]
+    bwd_ms = [bw.elapsed_time(c) for _, _, c, bw in evs] if train else []
     tot = sum(step_ms)
     tot_search = sum(search_ms)
     if world > 1:
@@ -288,7 +308,7 @@ def run_ours(args, wl):
     sims_p = torch.empty((rows, L)).pin_memory()
     offs_p = torch.empty((rows, L, 3)).pin_memory()
     out_p = torch.empty(vid_h.shape).pin_memory()
-    use_pipe = not (sharded and world > 1)
+    use_pipe = not (sharded and world > 1) and not train
     if use_pipe:
         # the C-ABI host-buffer call (snls_pipeline_run): frame-chunked kernels overlapped
         # with the H2D input / D2H result copies; Q = K = V is one host buffer, copied once
@@ -304,10 +324,15 @@ def run_ours(args, wl):
             vd.copy_(vid_p, non_blocking=True)
             ffd.copy_(ff_p, non_blocking=True)
             bfd.copy_(bf_p, non_blocking=True)
-            v2, f2, b2 = SH.exchange(vd, plan), SH.exchange(ffd, plan), SH.exchange(bfd, plan)
-            S.shifted_nls_forward(v2, v2, f2, b2, cfg, ctx=ctx, check=False,
-                                  out=(sims, offs, None, wts), frames=frames)
+            v2, f2, b2 = vd, ffd, bfd
+            if sharded and world > 1:
+                v2, f2, b2 = SH.exchange(vd, plan), SH.exchange(ffd, plan), SH.exchange(bfd, plan)
+            res = S.shifted_nls_forward(v2, v2, f2, b2, cfg, ctx=ctx, check=False,
+                                        out=(sims, offs, chains if train else None, wts), frames=frames)
             S.wpsum(v2, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
+            if train:
+                S.wpsum_backward(g_out, counts, v2, wts, offs, cfg, ctx=ctx, check=False)
+                S.shifted_nls_backward(g_sims, res, v2, v2, ctx=ctx, check=False)
             sims_p.copy_(sims, non_blocking=True)
             offs_p.copy_(offs, non_blocking=True)
             out_p.copy_(out, non_blocking=True)
@@ -380,7 +405,8 @@ def run_ours(args, wl):
                                    if sharded else f"batch-sharded x{world} (no collective)"),
                    "l2": "flushed (512 MB memset) between timed steps"},
         "breakdown_ms": {"search_topl_softmax": tot_search / args.steps,
-                         "wpsum": statistics.mean(wpsum_ms)},
+                         "wpsum": statistics.mean(wpsum_ms),
+                         **({"backward": statistics.mean(bwd_ms)} if train else {})},
         "roofline": {"bound": "fp32", "kernel": "search_tiled_kernel",
                      "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak_tflops, "traffic": traffic,
@@ -425,11 +451,22 @@ def reference_sample(wl, crop):
               topl=wl["topl"], metric=wl["metric"], softmax_scale=wl["beta"])
     rows = T * ((H - 1) // cfg.stride0 + 1) * ((W - 1) // cfg.stride0 + 1)
 
+    train = wl.get("train", False)
+    if train:  # upstream gradients of the sims and of the aggregated video
+        L = cfg.topl
+        gs = R.uniform(wl["gs_seed"], -1, 1, rows * L).astype(np.float32).astype(np.float64)
+        gs = gs.reshape(rows, L)
+        go = R.uniform(wl["go_seed"], -1, 1, v.size).astype(np.float32).astype(np.float64)
+        go = go.reshape(v.shape)
+
     def run():
         t0 = time.perf_counter()
         r = R.search_fwd(v, v, ff, bf, cfg)
         w = R.softmax_rows(r["sims"], cfg.softmax_scale)
-        R.wpsum(v, w, r["offsets"], cfg)
+        _, counts = R.wpsum(v, w, r["offsets"], cfg)
+        if train:  # the reference's default (deterministic) backward
+            R.wpsum_bwd(go, counts, v, w, r["offsets"], cfg)
+            R.search_bwd(v, v, cfg, r["centers"], r["chains"], gs)
         return time.perf_counter() - t0
 
     return R, rows, run
@@ -448,7 +485,8 @@ def cpu_baseline(wl, budget_s=20.0):
     med = statistics.median(times)
     return {"value": rows / med, "unit": UNIT, "cores": R.lib.ref_max_threads(),
             "kind": "reference",
-            "sample": (f"reference snls::shifted_nls_forward + softmax_rows + wpsum (oracle/_ref, "
+            "sample": (f"reference snls::shifted_nls_forward + softmax_rows + wpsum"
+                       f"{' + wpsum_backward + shifted_nls_backward' if wl.get('train') else ''} (oracle/_ref, "
                        f"fp64, OpenMP all host threads) on a {wl['T']}x{crop}x{crop}x{wl['C']} crop "
                        f"of the workload ({rows} queries, identical per-query work), median of "
                        f"{len(times)} runs after 1 warm-up ({t:.2f}s)")}

@@ -624,6 +624,138 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
     atomicAdd(dw + e, dw_acc);
 }
 
+// Row-centric wpsum backward (aggregate.cpp:351-460): one warp per (query row, 32-channel
+// slice), lane = channel.  Every write of a query (footprint pixel, or cell-completion
+// pixel through its clamped patch pixel, aggregate.cpp:80-100) samples V at a patch pixel
+// (i, j) of that query, so the upstream gradient is first folded per patch pixel:
+// Gs[i][j] = sum over the writes mapped to (i, j) of grad_out / count -- independent of the
+// neighbour l.  Then per neighbour: dW = sum Gs * sample (warp-reduced, one atomic per
+// slice) and dV gets w * Gs through the taps, pre-reduced on the (ps+1)^2 raw block two rows
+// at a time ((ps+1)^2 coalesced atomics per entry instead of 4 x writes).
+template <int P>
+__global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float* __restrict__ go,
+                                                         const int32_t* __restrict__ counts,
+                                                         float* __restrict__ dv, float* __restrict__ dw) {
+    constexpr int HP = P / 2;
+    const int slices = (a.d.f + 31) / 32;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= a.d.rows * slices) return;  // warp-uniform
+    const int64_t row = wid / slices;
+    const int c = int(wid % slices) * 32 + lane;
+    const bool act = c < a.d.f;
+    const int cc = act ? c : 0;
+    int ti, qy, qx;
+    row_coords(a.d, row, ti, qy, qx);
+    const int H = a.d.h, W = a.d.w, st = a.d.stride0;
+    const size_t F = size_t(a.d.f), rowF = size_t(W) * F, frameF = size_t(H) * rowF;
+    // ---- fold the upstream gradient onto the patch pixels
+    float gs[P][P];
+    const float* gob = go + size_t(ti) * frameF + cc;
+    const int32_t* cb = counts + size_t(ti) * H * W;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const int y = qy + i - HP, x = qx + j - HP;
+            float v = 0.f;
+            if (act && y >= 0 && y < H && x >= 0 && x < W) {
+                const int pix = y * W + x;
+                v = __ldg(gob + size_t(pix) * F) * (1.f / float(__ldg(cb + pix)));
+            }
+            gs[i][j] = v;
+        }
+    int ylo, yhi, xlo, xhi;  // the query's stride cell (aggregate.cpp:68-100)
+    cell_span(qy / st, st, a.d.nh, H, ylo, yhi);
+    cell_span(qx / st, st, a.d.nw, W, xlo, xhi);
+    if (ylo < qy - HP || yhi > qy + HP || xlo < qx - HP || xhi > qx + HP) {  // cell completion
+        for (int y = ylo; y <= yhi; ++y)
+            for (int x = xlo; x <= xhi; ++x) {
+                if (abs(y - qy) <= HP && abs(x - qx) <= HP) continue;
+                const int pi = clampi(y - qy, HP) + HP, pj = clampi(x - qx, HP) + HP;
+                const int pix = y * W + x;
+                const float v = act ? __ldg(gob + size_t(pix) * F) * (1.f / float(__ldg(cb + pix))) : 0.f;
+#pragma unroll
+                for (int i = 0; i < P; ++i)
+#pragma unroll
+                    for (int j = 0; j < P; ++j) gs[i][j] += (i == pi && j == pj) ? v : 0.f;
+            }
+    }
+    // ---- per neighbour: dW and the dV block scatter
+    for (int l = 0; l < a.topl; ++l) {
+        const int64_t e = row * a.topl + l;
+        const float* o = a.offsets + size_t(e) * 3;
+        const int kt = ti + int(roundf(__ldg(o)));
+        if (kt < 0 || kt >= a.d.t) {  // "offsets leave the clip" (aggregate.cpp:108-109)
+            if (lane == 0) latch(a.err, kErrWpsum);
+            continue;
+        }
+        const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+        const float fly = floorf(oy), flx = floorf(ox);
+        const float fy = oy - fly, fx = ox - flx;
+        const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+        const float w10 = fy * (1.f - fx), w11 = fy * fx;
+        const float wv = __ldg(a.weights + e);
+        const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+        unsigned bcol[P + 1];
+#pragma unroll
+        for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);
+        const float* vb = a.v + size_t(kt) * frameF + cc;
+        float* dvb = dv + size_t(kt) * frameF + cc;
+        float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
+        size_t roa = size_t(reflect_near(by, H)) * rowF;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) {
+            ra[j] = act ? __ldg(vb + roa + bcol[j]) : 0.f;
+            ka[j] = 0.f;
+        }
+        float dwl = 0.f;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const size_t rob = size_t(reflect_near(by + i + 1, H)) * rowF;
+#pragma unroll
+            for (int j = 0; j <= P; ++j) {
+                rb[j] = act ? __ldg(vb + rob + bcol[j]) : 0.f;
+                kn[j] = 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const float smp = w00 * ra[j] + w01 * ra[j + 1] + w10 * rb[j] + w11 * rb[j + 1];
+                dwl = fmaf(gs[i][j], smp, dwl);
+                const float gv = gs[i][j] * wv;
+                ka[j] += gv * w00;
+                ka[j + 1] += gv * w01;
+                kn[j] += gv * w10;
+                kn[j + 1] += gv * w11;
+            }
+            if (act) {
+#pragma unroll
+                for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + bcol[j], ka[j]);
+            }
+#pragma unroll
+            for (int j = 0; j <= P; ++j) {
+                ra[j] = rb[j];
+                ka[j] = kn[j];
+            }
+            roa = rob;
+        }
+        if (act) {
+#pragma unroll
+            for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + bcol[j], ka[j]);
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) dwl += __shfl_xor_sync(0xffffffffu, dwl, m);
+        if (lane == 0) atomicAdd(dw + e, dwl);
+    }
+}
+
+template <int P>
+void launch_wpsum_bwd_rows(const AggArgs& a, const float* go, const int32_t* counts, float* dv,
+                           float* dw, cudaStream_t st) {
+    const int64_t warps = a.d.rows * ((a.d.f + 31) / 32);
+    wpsum_bwd_rows<P><<<unsigned((warps + 3) / 4), 128, 0, st>>>(a, go, counts, dv, dw);
+}
+
 }  // namespace
 
 int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* weights, int* err,
@@ -661,6 +793,13 @@ int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st) {
 
 int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                      float* dw, cudaStream_t st) {
+    switch (a.ps) {
+        case 1: launch_wpsum_bwd_rows<1>(a, grad_out, counts, dv, dw, st); return 1;
+        case 3: launch_wpsum_bwd_rows<3>(a, grad_out, counts, dv, dw, st); return 1;
+        case 5: launch_wpsum_bwd_rows<5>(a, grad_out, counts, dv, dw, st); return 1;
+        case 7: launch_wpsum_bwd_rows<7>(a, grad_out, counts, dv, dw, st); return 1;
+        default: break;
+    }
     if (a.d.f % 4 == 0) {
         const int64_t n = a.d.rows * a.topl * (a.d.f / 4);
         wpsum_bwd_kernel<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, grad_out, counts, dv, dw);

@@ -1,6 +1,7 @@
 // Search backward (shifted_nls_backward, search.cpp:499-711) on device.
 //
-// Phase 1: one thread per (selected entry, channel group).  It replays the entry's patch
+// Phase 1 (ps <= 7: search_bwd_rows, register pre-reduction; else search_bwd_entries):
+// one thread per (selected entry, channel group).  It replays the entry's patch
 // (same taps as the forward), scatters dQ into the reflected query pixels and dK into the
 // 4 bilinear taps with atomics, and accumulates its share of dS/d(ky, kx) in fp64.  The
 // per-entry (gy, gx) is reduced across the channel-group threads with fp64 atomics.
@@ -89,6 +90,152 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
     atomicAdd(gyx + 2 * e + 1, gx);
 }
 
+// Row-centric backward (any stride1: every pixel of one entry's patch shares the
+// fractional offset frac(offset), so its 4 ps^2 taps fall on one (ps+1)^2 raw block):
+// one warp per (query row, 32-channel slice), lane = channel.  Same per-(pixel, channel)
+// arithmetic as search_bwd_entries, with the scatter pre-reduced in registers before the
+// atomics: dQ is summed over the row's L entries (ps^2 atomics per row instead of L ps^2),
+// dK is accumulated on the raw block two rows at a time ((ps+1)^2 atomics per entry instead
+// of 4 ps^2), and dS/d(ky, kx) is warp-reduced (one fp64 atomic pair per slice).  Every
+// atomic is a fully coalesced 128 B warp access along the channels.
+template <int P>
+__global__ void __launch_bounds__(128, 3) search_bwd_rows(const float* __restrict__ grad,
+                                                          const float* __restrict__ offsets,
+                                                          const float* __restrict__ q,
+                                                          const float* __restrict__ k, Dims d,
+                                                          int topl, int metric, float* dq,
+                                                          float* dk, double* gyx) {
+    constexpr int HP = P / 2;
+    const int slices = (d.f + 31) / 32;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= d.rows * slices) return;  // warp-uniform
+    const int64_t row = wid / slices;
+    const int c = int(wid % slices) * 32 + lane;
+    const bool act = c < d.f;
+    const int cc = act ? c : 0;
+    int qt, qy, qx;
+    row_coords(d, row, qt, qy, qx);
+    const size_t F = size_t(d.f), rowF = size_t(d.w) * F, frameF = size_t(d.h) * rowF;
+    int qrow[P], qcol[P];  // reflected query pixels (search.cpp:129-132)
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        qrow[p] = reflect_near(qy + p - HP, d.h) * d.w;
+        qcol[p] = reflect_near(qx + p - HP, d.w);
+    }
+    const float* qb = q + size_t(qt) * frameF + cc;
+    float dqa[P][P];
+#pragma unroll
+    for (int py = 0; py < P; ++py)
+#pragma unroll
+        for (int px = 0; px < P; ++px) dqa[py][px] = 0.f;
+
+    for (int l = 0; l < topl; ++l) {
+        const int64_t e = row * topl + l;
+        const float g = __ldg(grad + e);
+        if (g == 0.f) continue;  // search.cpp:692 (uniform: one row per warp)
+        const float* o = offsets + size_t(e) * 3;
+        const int kt = qt + int(rintf(__ldg(o)));
+        const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+        const float fly = floorf(oy), flx = floorf(ox);
+        const float fy = oy - fly, fx = ox - flx;
+        const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+        const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+        const float w10 = fy * (1.f - fx), w11 = fy * fx;
+        unsigned bcol[P + 1];
+#pragma unroll
+        for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, d.w)) * unsigned(d.f);
+        const float* kb = k + size_t(kt) * frameF + cc;
+        float* dkb = dk + size_t(kt) * frameF + cc;
+        float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
+        size_t roa = size_t(reflect_near(by, d.h)) * rowF;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) {
+            ra[j] = act ? __ldg(kb + roa + bcol[j]) : 0.f;
+            ka[j] = 0.f;
+        }
+        double sy = 0.0, sx = 0.0;
+#pragma unroll
+        for (int py = 0; py < P; ++py) {
+            const size_t rob = size_t(reflect_near(by + py + 1, d.h)) * rowF;
+#pragma unroll
+            for (int j = 0; j <= P; ++j) {
+                rb[j] = act ? __ldg(kb + rob + bcol[j]) : 0.f;
+                kn[j] = 0.f;
+            }
+            float ry = 0.f, rx = 0.f;  // this patch row's share of dS/d(ky, kx)
+#pragma unroll
+            for (int px = 0; px < P; ++px) {
+                const float k00 = ra[px], k01 = ra[px + 1], k10 = rb[px], k11 = rb[px + 1];
+                const float qv = act ? __ldg(qb + size_t(qrow[py] + qcol[px]) * F) : 0.f;
+                const float kv = fmaf(w11, k11, fmaf(w10, k10, fmaf(w01, k01, w00 * k00)));
+                float ds_dq, ds_dk;
+                if (metric == SNLS_METRIC_IP) {
+                    ds_dq = kv;
+                    ds_dk = qv;
+                } else {
+                    const float diff = qv - kv;
+                    ds_dq = -2.f * diff;
+                    ds_dk = 2.f * diff;
+                }
+                const float gk = g * ds_dk;
+                dqa[py][px] = fmaf(g, ds_dq, dqa[py][px]);
+                ka[px] = fmaf(gk, w00, ka[px]);
+                ka[px + 1] = fmaf(gk, w01, ka[px + 1]);
+                kn[px] = fmaf(gk, w10, kn[px]);
+                kn[px + 1] = fmaf(gk, w11, kn[px + 1]);
+                // d(sample)/dy, d(sample)/dx from the tap values (search.cpp:574-577)
+                const float dkv_dy = (1.f - fx) * (k10 - k00) + fx * (k11 - k01);
+                const float dkv_dx = (1.f - fy) * (k01 - k00) + fy * (k11 - k10);
+                ry = fmaf(gk, dkv_dy, ry);
+                rx = fmaf(gk, dkv_dx, rx);
+            }
+            // dS/d(ky, kx) sums thousands of cancelling terms per entry: the per-row partials
+            // are accumulated in fp64
+            sy += double(ry);
+            sx += double(rx);
+            if (act) {  // raw row py of the block is complete
+#pragma unroll
+                for (int j = 0; j <= P; ++j) atomicAdd(dkb + roa + bcol[j], ka[j]);
+            }
+#pragma unroll
+            for (int j = 0; j <= P; ++j) {
+                ra[j] = rb[j];
+                ka[j] = kn[j];
+            }
+            roa = rob;
+        }
+        if (act) {
+#pragma unroll
+            for (int j = 0; j <= P; ++j) atomicAdd(dkb + roa + bcol[j], ka[j]);
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            sy += __shfl_xor_sync(0xffffffffu, sy, m);
+            sx += __shfl_xor_sync(0xffffffffu, sx, m);
+        }
+        if (lane == 0) {
+            atomicAdd(gyx + 2 * e, sy);
+            atomicAdd(gyx + 2 * e + 1, sx);
+        }
+    }
+    if (act) {
+        float* dqb = dq + size_t(qt) * frameF + cc;
+#pragma unroll
+        for (int py = 0; py < P; ++py)
+#pragma unroll
+            for (int px = 0; px < P; ++px) atomicAdd(dqb + size_t(qrow[py] + qcol[px]) * F, dqa[py][px]);
+    }
+}
+
+template <int P>
+void launch_rows(const float* grad, const float* offsets, const float* q, const float* k, Dims d,
+                 int topl, int metric, float* dq, float* dk, double* gyx, cudaStream_t st) {
+    const int64_t warps = d.rows * ((d.f + 31) / 32);
+    search_bwd_rows<P><<<unsigned((warps + 3) / 4), 128, 0, st>>>(grad, offsets, q, k, d, topl, metric,
+                                                                  dq, dk, gyx);
+}
+
 __global__ void search_bwd_route(const float* __restrict__ grad,
                                  const float* __restrict__ offsets,
                                  const float* __restrict__ chains, Dims d, int wt, int topl,
@@ -156,7 +303,14 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
     double* dbf64 = dff64 + nfl;
     const int vec = d.f % 4 == 0 ? 4 : 1;
     const int64_t n = d.rows * topl * (d.f / vec);
-    if (vec == 4)
+    if (ps == 1 || ps == 3 || ps == 5 || ps == 7) {
+        switch (ps) {
+            case 1: launch_rows<1>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
+            case 3: launch_rows<3>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
+            case 5: launch_rows<5>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
+            default: launch_rows<7>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
+        }
+    } else if (vec == 4)
         search_bwd_entries<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps,
                                                                          topl, metric, dq, dk, gyx);
     else

@@ -222,8 +222,14 @@ def run_ours(args, wl):
     own_ff = torch.from_numpy(ff_h).to(dev)
     own_bf = torch.from_numpy(bf_h).to(dev)
     vid, ff, bf = own_vid, own_ff, own_bf
-    if sharded:  # slab buffers (the exchange refills them every step when world > 1)
-        vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
+    if sharded:  # persistent slabs [lo, hi): owned frames in place, halo frames refilled by
+        # the in-place NCCL exchange every step (overlapped with the interior frames)
+        def slab_of(own):
+            sl = torch.zeros((plan.hi - plan.lo,) + tuple(own.shape[1:]), device=dev)
+            sl[plan.t0:plan.t1].copy_(own)
+            return sl
+        vid, ff, bf = slab_of(own_vid), slab_of(own_ff), slab_of(own_bf)
+    overlapped = sharded and world > 1
     stream = torch.cuda.current_stream(dev)
     ctx = S.context(local)
     ctx.set_search_kernel(args.search_kernel)
@@ -243,9 +249,11 @@ def run_ours(args, wl):
     bwd_ms = []
 
     def step():
-        nonlocal vid, ff, bf
-        if sharded and world > 1:  # the data path's only communication: the wt-frame halo
-            vid, ff, bf = SH.exchange(own_vid, plan), SH.exchange(own_ff, plan), SH.exchange(own_bf, plan)
+        if overlapped:  # the data path's only communication: the wt-frame halo (NCCL P2P)
+            SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, world=world,
+                                           out=(sims, offs, None, wts, out, counts))
+            ev_mid.record(stream)
+            return
         res = S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
                                     out=(sims, offs, chains if train else None, wts), frames=frames)
         ev_mid.record(stream)
@@ -325,8 +333,16 @@ def run_ours(args, wl):
             ffd.copy_(ff_p, non_blocking=True)
             bfd.copy_(bf_p, non_blocking=True)
             v2, f2, b2 = vd, ffd, bfd
-            if sharded and world > 1:
-                v2, f2, b2 = SH.exchange(vd, plan), SH.exchange(ffd, plan), SH.exchange(bfd, plan)
+            if overlapped:
+                vid[plan.t0:plan.t1].copy_(vd)
+                ff[plan.t0:plan.t1].copy_(ffd)
+                bf[plan.t0:plan.t1].copy_(bfd)
+                SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, world=world,
+                                               out=(sims, offs, None, wts, out, counts))
+                sims_p.copy_(sims, non_blocking=True)
+                offs_p.copy_(offs, non_blocking=True)
+                out_p.copy_(out, non_blocking=True)
+                return
             res = S.shifted_nls_forward(v2, v2, f2, b2, cfg, ctx=ctx, check=False,
                                         out=(sims, offs, chains if train else None, wts), frames=frames)
             S.wpsum(v2, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
@@ -404,7 +420,8 @@ def run_ours(args, wl):
                    "parallelism": (f"frame-sharded x{world}, wt-frame halo via NCCL send/recv"
                                    if sharded else f"batch-sharded x{world} (no collective)"),
                    "l2": "flushed (512 MB memset) between timed steps"},
-        "breakdown_ms": {"search_topl_softmax": tot_search / args.steps,
+        "breakdown_ms": {("search_topl_softmax" if not overlapped else
+                          "search_softmax_wpsum_with_halo_exchange"): tot_search / args.steps,
                          "wpsum": statistics.mean(wpsum_ms),
                          **({"backward": statistics.mean(bwd_ms)} if train else {})},
         "roofline": {"bound": "fp32", "kernel": "search_tiled_kernel",

@@ -340,8 +340,15 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
         return fail(SNLS_ECONFIG, "search: topl exceeds the valid window entries of some query");
     DeviceGuard g(ctx->device);
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
-    const int64_t nflow = int64_t(dims.t) * dims.h * dims.w * 2;
-    int launched = launch_flows_check(ff, bf, nflow, ctx->err, ctx->stream);
+    // validate_forward_inputs (search.cpp:175-183) checks every flow frame; a frame range
+    // checks the frames its queries can read, [t0 - wt, t1 + wt) -- the whole clip for the
+    // plain entry, and a shard's halo frames are checked by their owner (they may still be
+    // in flight while the interior frames run)
+    const int f0 = t0 - cfg->wt > 0 ? t0 - cfg->wt : 0;
+    const int f1 = t1 + cfg->wt < dims.t ? t1 + cfg->wt : dims.t;
+    const int64_t fframe = int64_t(dims.h) * dims.w * 2;
+    int launched = launch_flows_check(ff ? ff + f0 * fframe : nullptr, bf ? bf + f0 * fframe : nullptr,
+                                      (f1 - f0) * fframe, ctx->err, ctx->stream);
     const float beta = float(cfg->softmax_scale);
 
     if (mode == SNLS_MODE_FULLGRID) {

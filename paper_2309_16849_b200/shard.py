@@ -90,6 +90,67 @@ def exchange(local, p: ShardPlan, group=None):
     return slab
 
 
+def exchange_async(slabs, p: ShardPlan, group=None):
+    """Fill the halo frames of persistent slab tensors in place: every tensor in `slabs` is a
+    frame-major [lo, hi) slab whose owned frames [a, b) are already in place; one batched
+    send/recv per (peer, direction, tensor) is started and the work handles are returned
+    (NCCL: wait() only orders the caller's stream after the transfer, so work enqueued
+    before it -- the interior frames -- overlaps the exchange)."""
+    import torch.distributed as dist
+
+    ops = []
+    for slab in slabs:
+        for peer, (lo, hi), kind in transfers(p):
+            view = slab[lo - p.lo:hi - p.lo]
+            ops.append(dist.P2POp(dist.irecv if kind == "recv" else dist.isend, view, peer, group))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def interior_range(p: ShardPlan):
+    """Owned query frames whose key/value/flow frames all lie in the owned range (no halo
+    needed): [a + wt, b - wt) -- chain links read fflow qt..qt+dt-1 and bflow qt..qt+dt+1
+    (search.cpp:84-101), wpsum reads v at qt + dt (aggregate.cpp:108)."""
+    lo = min(p.a + p.wt, p.b)
+    hi = max(p.b - p.wt, lo)
+    return lo, hi
+
+
+def search_aggregate_overlapped(slab_q, slab_k, slab_v, slab_ff, slab_bf, p: ShardPlan, cfg, out,
+                                ctx=None, group=None, world=1, split=None):
+    """One frame-sharded step with the halo exchange overlapped: start the exchange of the
+    K/V/flow halo, search + aggregate the interior frames (no halo needed) meanwhile, wait,
+    then do the edge frames.  `out` = (sims, offsets, chains, weights, video, counts) for
+    the owned frames; the slabs are persistent [lo, hi) tensors with the owned frames in
+    place (Q only needs its owned frames)."""
+    from . import snls as S
+
+    sims, offs, chains, wts, vout, counts = out
+    uniq = []  # aliased slabs (Q = K = V) are exchanged once
+    for x in (slab_k, slab_v, slab_ff, slab_bf):
+        if all(x is not u for u in uniq):
+            uniq.append(x)
+    reqs = exchange_async(uniq, p, group) if world > 1 else []
+    nq = sims.shape[0] // (p.b - p.a)
+
+    def run(f0, f1):  # owned query frames [f0, f1)
+        if f0 >= f1:
+            return
+        r0, r1 = (f0 - p.a) * nq, (f1 - p.a) * nq
+        o = (sims[r0:r1], offs[r0:r1], None if chains is None else chains[r0:r1], wts[r0:r1])
+        S.shifted_nls_forward(slab_q, slab_k, slab_ff, slab_bf, cfg, ctx=ctx, check=False, out=o,
+                              frames=(f0 - p.lo, f1 - p.lo))
+        S.wpsum(slab_v, wts[r0:r1], offs[r0:r1], cfg, ctx=ctx, check=False,
+                out=(vout[f0 - p.a:f1 - p.a], counts[f0 - p.a:f1 - p.a]), frames=(f0 - p.lo, f1 - p.lo))
+
+    split = world > 1 if split is None else split
+    ia, ib = interior_range(p) if split else (p.a, p.b)
+    run(ia, ib)
+    for r in reqs:
+        r.wait()
+    run(p.a, ia)
+    run(ib, p.b)
+
+
 def search_aggregate_shard(q_local, k_slab, v_slab, ff_slab, bf_slab, p: ShardPlan, cfg, ctx=None,
                            check=True):
     """Search + fused softmax + wpsum for the owned frames on the device (C-ABI frame-range

@@ -34,3 +34,36 @@ def test_slab_equals_unsharded(F, ps, ws, wt):
             assert np.array_equal(host(res.weights), host(full.weights)[rows])
             assert np.array_equal(host(out), host(fout)[p.a:p.b])
             assert np.array_equal(host(cnt), host(fcnt)[p.a:p.b])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_overlapped_interior_then_edges_equals_unsharded(world):
+    """The overlapped step (interior frames first, then the halo-dependent edge frames, each
+    through the frame-range entry points) reproduces the unsharded rows bit for bit; the
+    slabs are prefilled as the exchange would leave them."""
+    import torch
+
+    S = snls_mod()
+    P = Checker("port")
+    T, H, W, F = 11, 18, 20, 32
+    cfg = S.SearchConfig(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2", softmax_scale=1 / 288)
+    v = video(P, T, H, W, F, 21)
+    ff, bf = flow(P, T, H, W, 22, 2.0), flow(P, T, H, W, 23, 2.0)
+    full = S.shifted_nls_forward(dev(v), dev(v), dev(ff), dev(bf), cfg, want_weights=True)
+    fout, fcnt = S.wpsum(dev(v), full.weights, full.offsets, cfg)
+    nq = ((H - 1) // 2 + 1) * ((W - 1) // 2 + 1)
+    for rank in range(world):
+        p = shard.plan(T, world, rank, cfg.wt)
+        n = (p.b - p.a) * nq
+        o = (torch.empty((n, 10), device="cuda"), torch.empty((n, 10, 3), device="cuda"), None,
+             torch.empty((n, 10), device="cuda"), torch.empty((p.b - p.a, H, W, F), device="cuda"),
+             torch.empty((p.b - p.a, H, W), device="cuda", dtype=torch.int32))
+        sl = lambda x: dev(x[p.lo:p.hi])  # noqa: E731
+        vs = sl(v)
+        shard.search_aggregate_overlapped(vs, vs, vs, sl(ff), sl(bf), p, cfg, o, split=True)
+        rows = slice(p.a * nq, p.b * nq)
+        assert np.array_equal(host(o[0]), host(full.sims)[rows])
+        assert np.array_equal(host(o[1]), host(full.offsets)[rows])
+        assert np.array_equal(host(o[3]), host(full.weights)[rows])
+        assert np.array_equal(host(o[4]), host(fout)[p.a:p.b])
+        assert np.array_equal(host(o[5]), host(fcnt)[p.a:p.b])

@@ -108,3 +108,52 @@ def test_gloo_halo_exchange_matches_unsharded_oracle(tmp_path, world, T):
         assert np.array_equal(z["sims"], full["sims"][a * nq:b * nq])   # bitwise, not approx
         assert np.array_equal(z["offsets"], full["offsets"][a * nq:b * nq])
         assert np.array_equal(z["out"], fout[a:b]) and np.array_equal(z["counts"], fcounts[a:b])
+
+
+def test_interior_range_needs_no_halo():
+    for T in (6, 9, 64):
+        for world in (2, 3, 8):
+            if world > T:
+                continue
+            for wt in (1, 2, 3):
+                for r in range(world):
+                    p = shard.plan(T, world, r, wt)
+                    ia, ib = shard.interior_range(p)
+                    assert p.a <= ia <= ib <= p.b
+                    for qt in range(ia, ib):  # every frame a query can read is owned
+                        assert p.a <= qt - wt and qt + wt < p.b
+
+
+def _async_worker(rank, world, port, T, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_16849_b200 import shard as SH
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    p = SH.plan(T, world, rank, 2)
+    full = torch.arange(T * 6, dtype=torch.float32).reshape(T, 3, 2) + 0.5
+    slab = torch.full((p.hi - p.lo, 3, 2), -1.0)
+    slab[p.t0:p.t1] = full[p.a:p.b]
+    flow = torch.full((p.hi - p.lo, 3, 2), -2.0)
+    flow[p.t0:p.t1] = -full[p.a:p.b]
+    for r in SH.exchange_async([slab, flow], p):
+        r.wait()
+    np.savez(os.path.join(out_dir, f"a{rank}.npz"), slab=slab.numpy(), flow=flow.numpy(),
+             want=full[p.lo:p.hi].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T", [(2, 6), (3, 7), (4, 9)])
+def test_gloo_inplace_async_exchange(tmp_path, world, T):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_async_worker, args=(world, _free_port(), T, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        z = np.load(tmp_path / f"a{r}.npz")
+        assert np.array_equal(z["slab"], z["want"]) and np.array_equal(z["flow"], -z["want"])

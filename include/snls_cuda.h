@@ -91,8 +91,8 @@ int snls_ctx_launch_count(snls_ctx* ctx, int64_t* out);
 int snls_ctx_last_search_path(snls_ctx* ctx, int* out);
 /* Force the generic per-slot search path (1) or allow the tiled one (0, default). */
 int snls_ctx_force_generic(snls_ctx* ctx, int on);
-/* stride1 == 1 register plan: 0 auto (streaming where instantiated, else tiled),
- * 1 region-row tiled, 2 streaming.  Results agree to the parity tolerance; each plan is
+/* stride1 == 1 register plan: 0 auto (= region-row tiled), 1 region-row tiled,
+ * 2 query-stationary streaming (ps in {3, 7}, F in {32, 64}; else tiled).  Results agree to the parity tolerance; each plan is
  * deterministic and tie-exact on its own. */
 int snls_ctx_set_search_kernel(snls_ctx* ctx, int kind);
 

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "search_select.cuh"
 
 namespace snls_gpu {
 
@@ -31,61 +32,17 @@ namespace {
 constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
 constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
-template <int VEC>
-__device__ __forceinline__ void ldv(const float* p, float (&o)[VEC]) {
-    if constexpr (VEC == 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-    } else if constexpr (VEC == 2) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-        o[0] = v.x; o[1] = v.y;
-    } else {
-        o[0] = __ldg(p);
-    }
-}
-
-template <int P, int W, int VEC, int G, int KMAX>
+template <int P, int W, int VEC, int G>
 struct StreamCfg {
     static constexpr int HP = P / 2, HW = W / 2, R = W + P - 1, F = G * VEC;
     static constexpr int QPW = 32 / G, WARPS = 4, QPB = QPW * WARPS;
-    static constexpr int M = KMAX / G > 0 ? KMAX / G : 1;  // list ranks per lane
-    // reduce-scatter geometry: W slots padded to NPAD; if NPAD >= G every lane ends with
-    // NPL consecutive slots, else 2^SH neighbouring lanes share one slot (all-reduced)
-    static constexpr int NPAD = pow2ceil(W);
-    static constexpr int NPL = NPAD >= G ? NPAD / G : 1;
-    static constexpr int SH = NPAD >= G ? 0 : ilog2(G / NPAD);
 };
-
-// Rank-sharded group list (see search_tiled.cu group_insert): lane gl holds ranks
-// [gl*M, gl*M+M) sorted descending; strict '>' keeps earlier slots ahead on ties.
-template <int G, int M>
-__device__ __forceinline__ void list_insert(float (&ev)[M], uint32_t (&es)[M], float v, uint32_t s,
-                                            int gl) {
-    float pv = __shfl_up_sync(0xffffffffu, ev[M - 1], 1, G);
-    uint32_t ps = __shfl_up_sync(0xffffffffu, es[M - 1], 1, G);
-    if (gl == 0) pv = INFINITY;
-    float nv[M];
-    uint32_t ns[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const float above = j == 0 ? pv : ev[j - 1];
-        const uint32_t above_s = j == 0 ? ps : es[j - 1];
-        const bool ga = v > above, gc = v > ev[j];
-        nv[j] = ga ? above : (gc ? v : ev[j]);
-        ns[j] = ga ? above_s : (gc ? s : es[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        ev[j] = nv[j];
-        es[j] = ns[j];
-    }
-}
 
 template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB>
 __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a) {
     static_assert(W >= P, "window narrower than the patch: not instantiated");
-    using C = StreamCfg<P, W, VEC, G, KMAX>;
-    constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F, M = C::M;
+    using C = StreamCfg<P, W, VEC, G>;
+    constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
     __shared__ uint64_t s_keys[C::QPB][16];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -114,24 +71,15 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
         }
     }
 
-    float ev[M];
-    uint32_t es[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        ev[j] = -INFINITY;
-        es[j] = 0xffffffffu;
-    }
-    // rank topl-1 of the group list is the selection threshold
-    const int thr_lane = (lane / G) * G + (a.topl - 1) / M, thr_idx = (a.topl - 1) % M;
+    TopL<W, G, KMAX> sel;
+    sel.init();
+    float* grid_row = a.grid ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
         const int dt = scan_dt(fp), kt = qt + dt;
         const bool on = row_ok && kt >= 0 && kt < a.d.t;
         if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
-            if (a.grid && row_ok) {
-                float* g = a.grid + size_t(row) * nfr * W * W + size_t(fp) * W * W;
-                for (int s = gl; s < W * W; s += G) g[s] = -INFINITY;
-            }
+            if (a.grid && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
             continue;
         }
         double sdy = 0.0, sdx = 0.0;
@@ -201,70 +149,9 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
             }
 
             // ---- slot row r-(P-1) complete: reduce-scatter over the G lanes, then stream
-            if (r >= P - 1) {
-                float v[C::NPAD];
-#pragma unroll
-                for (int b = 0; b < C::NPAD; ++b) v[b] = b < W ? acc[0][b] : 0.f;
-                // scatter levels: the lane bit for m picks the upper half of the values
-#pragma unroll
-                for (int lev = 0; lev < ilog2(G); ++lev) {
-                    const int m = G >> (lev + 1), n = C::NPAD >> lev;  // n values before
-                    if (n > 1) {
-                        const bool hi = (gl & m) != 0;
-#pragma unroll
-                        for (int i = 0; i < n / 2; ++i) {
-                            const float keep = hi ? v[i + n / 2] : v[i];
-                            const float send = hi ? v[i] : v[i + n / 2];
-                            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-                        }
-                    } else {  // more lanes than slots: all-reduce the remaining levels
-                        v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
-                    }
-                }
-                const int arow = r - (P - 1);
-                // lane gl holds slots (gl >> SH) * NPL + i, i < NPL; owner lanes have the
-                // low SH bits clear
-                const int sb = (gl >> C::SH) * C::NPL;
-                const bool owner = (gl & ((1 << C::SH) - 1)) == 0;
-                if (a.grid) {  // kFullGrid: materialise the scores (-inf off-clip), no selection
-#pragma unroll
-                    for (int i = 0; i < C::NPL; ++i) {
-                        const int b = sb + i;
-                        const float val = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
-                        if (row_ok && owner && b < W)
-                            a.grid[size_t(row) * nfr * W * W + slot_base + arow * W + b] = on ? val : -INFINITY;
-                    }
-                } else {
-                    float thr = -INFINITY;
-#pragma unroll
-                    for (int j = 0; j < M; ++j) thr = j == thr_idx ? ev[j] : thr;
-                    thr = __shfl_sync(0xffffffffu, thr, thr_lane);
-                    uint32_t pend = 0;
-#pragma unroll
-                    for (int i = 0; i < C::NPL; ++i) {
-                        const int b = sb + i;
-                        v[i] = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];
-                        if (on && owner && b < W && v[i] > thr) pend |= 1u << i;
-                    }
-                    // survivors one at a time, lanes then slots ascending (= slot order)
-                    while (__any_sync(0xffffffffu, pend != 0)) {
-                        const unsigned want = __ballot_sync(0xffffffffu, pend != 0);
-                        const unsigned gmask =
-                            (want >> (gq * G)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
-                        const int src = gmask ? gq * G + (__ffs(gmask) - 1) : lane;
-                        const int isrc = pend ? (__ffs(pend) - 1) : 0;
-                        float cv = -INFINITY;
-#pragma unroll
-                        for (int i = 0; i < C::NPL; ++i) cv = (i == isrc) ? v[i] : cv;
-                        const uint32_t cs = slot_base + uint32_t(arow * W + sb + isrc);
-                        float bv = __shfl_sync(0xffffffffu, cv, src);
-                        const uint32_t bs = __shfl_sync(0xffffffffu, cs, src);
-                        if (!gmask) bv = -INFINITY;  // keeps the shuffles warp-uniform
-                        list_insert<G, M>(ev, es, bv, bs, gl);
-                        if (lane == src && gmask) pend &= pend - 1;
-                    }
-                }
-            }
+            if (r >= P - 1)
+                sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base,
+                                                grid_row, a.topl);
             // rotate: acc[s] tracks slot row r-(P-1)+s
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)
@@ -276,70 +163,12 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
     }
 
     if (a.grid) return;  // selection happens in the top_l pass over the grid
-
-    // ---- lane gl owns ranks gl*M .. gl*M+M-1 of the merged list
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const int li = gl * M + j;
-        if (li < a.topl) s_keys[qslot][li] = eligible(ev[j]) ? pack_key(ev[j], es[j]) : 0ull;
-    }
-    __syncwarp();
-
-    // ---- emit_row (search.cpp:207-234) + softmax epilogue (aggregate.cpp:16-37)
-    float zmax = -INFINITY;
-    for (int li = gl; row_ok && li < a.topl; li += G) {
-        const uint64_t key = s_keys[qslot][li];
-        const size_t e = size_t(row) * a.topl + li;
-        float v = -INFINITY, o1 = 0.f, o2 = 0.f;
-        int dt = 0;
-        if (key != 0ull) {
-            const uint32_t slot = key_slot(key);
-            v = key_value(key);
-            const int fp = int(slot) / (W * W), rem = int(slot) % (W * W);
-            dt = scan_dt(fp);
-            double sdy, sdx;
-            shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
-            const double ky = (double(qy) + sdy) + double(rem / W - HW);
-            const double kx = (double(qx) + sdx) + double(rem % W - HW);
-            o1 = float(ky - double(qy));
-            o2 = float(kx - double(qx));
-        }
-        a.sims[e] = v;
-        a.offsets[e * 3 + 0] = float(dt);
-        a.offsets[e * 3 + 1] = o1;
-        a.offsets[e * 3 + 2] = o2;
-        if (a.chains && a.wt > 1) {
-            const int cs = a.wt - 1;
-            float* lk = a.chains + e * size_t(cs) * 6;
-            for (int j = 0; j < cs * 6; ++j) lk[j] = 0.f;
-            if (dt > 1 || dt < -1) {
-                double sdy, sdx;
-                shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, lk);
-            }
-        }
-        zmax = fmaxf(zmax, a.beta * v);
-    }
-    if (a.weights) {
-#pragma unroll
-        for (int m = G / 2; m >= 1; m >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, m));
-        float sum = 0.f;
-        for (int li = gl; row_ok && li < a.topl; li += G) {
-            const float z = a.beta * key_value(s_keys[qslot][li]);
-            if (!isfinite(z)) latch(a.err, kErrSoftmax);
-            sum += __expf(z - zmax);
-        }
-#pragma unroll
-        for (int m = G / 2; m >= 1; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
-        for (int li = gl; row_ok && li < a.topl; li += G) {
-            const size_t e = size_t(row) * a.topl + li;
-            a.weights[e] = __expf(a.beta * key_value(s_keys[qslot][li]) - zmax) / sum;
-        }
-    }
+    sel.emit(a, s_keys[qslot], row, row_ok, gl, qt, qy, qx);
 }
 
 template <int P, int W, int VEC, int G, int MINB>
 int launch_one(const TiledSearch& s, cudaStream_t st) {
-    using C = StreamCfg<P, W, VEC, G, 16>;
+    using C = StreamCfg<P, W, VEC, G>;
     const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
     if (s.metric == SNLS_METRIC_IP)
         search_stream_kernel<P, W, VEC, G, 16, SNLS_METRIC_IP, MINB><<<blocks, 128, 0, st>>>(s);

@@ -145,6 +145,15 @@ int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                     const float* q, const float* k, float* dq, float* dk, float* dfflow,
                     float* dbflow);
 
+/* Frame-range form (frame sharding, reverse halo): the tape rows of query frames [t0, t1)
+ * only (grad_sims / offsets / chains hold those rows); dq, dk, dfflow, dbflow cover all
+ * dims.t frames of the caller's slab -- the parts in halo frames are partial sums the owner
+ * of those frames adds (paper_2309_16849_b200/shard.py reverse_exchange_add). */
+int snls_search_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                           const float* grad_sims, const float* offsets, const float* chains,
+                           const float* q, const float* k, float* dq, float* dk, float* dfflow,
+                           float* dbflow);
+
 /* ---- aggregate (aggregate.hpp) ------------------------------------------------------ */
 /* Replaces snls::softmax_rows (aggregate.hpp:22; aggregate.cpp:16-37). */
 int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims,
@@ -172,6 +181,13 @@ int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
 int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                    const float* grad_out, const int32_t* counts, const float* v,
                    const float* weights, const float* offsets, float* dv, float* dweights);
+
+/* Frame-range form: grad_out / counts hold output frames [t0, t1), weights / offsets / dw
+ * the rows of those frames; v and dv cover all dims.t frames (dv in halo frames: partial
+ * sums for their owner). */
+int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* grad_out, const int32_t* counts, const float* v,
+                          const float* weights, const float* offsets, float* dv, float* dweights);
 
 /* ---- host-buffer pipeline (the search -> softmax_rows -> wpsum core of align_frames /
  * run_benchmark, harness.cpp:105-154, 242-283, over HOST memory) ---------------------

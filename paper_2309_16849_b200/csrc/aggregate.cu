@@ -599,13 +599,13 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
             pyu = clampi(y - qy, half);
             pxu = clampi(x - qx, half);
         }
-        const float inv_cnt = 1.f / float(counts[(size_t(ti) * a.d.h + y) * a.d.w + x]);
+        const float inv_cnt = 1.f / float(counts[(size_t(ti - a.d.t0) * a.d.h + y) * a.d.w + x]);
         int iy, ix;
         float fy, fx;
         split_pos(qy + pyu, oy, iy, fy);
         split_pos(qx + pxu, ox, ix, fx);
         const Taps t = taps_from(iy, fy, ix, fx, a.d.h, a.d.w);
-        const float* gp = go + vidx(a.d, ti, y, x) + c;
+        const float* gp = go + vidx(a.d, ti - a.d.t0, y, x) + c;
         const size_t i00 = vidx(a.d, kt, t.y0, t.x0) + c, i01 = vidx(a.d, kt, t.y0, t.x1) + c;
         const size_t i10 = vidx(a.d, kt, t.y1, t.x0) + c, i11 = vidx(a.d, kt, t.y1, t.x1) + c;
 #pragma unroll
@@ -651,8 +651,9 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
     const size_t F = size_t(a.d.f), rowF = size_t(W) * F, frameF = size_t(H) * rowF;
     // ---- fold the upstream gradient onto the patch pixels
     float gs[P][P];
-    const float* gob = go + size_t(ti) * frameF + cc;
-    const int32_t* cb = counts + size_t(ti) * H * W;
+    // grad_out / counts hold the output frames [t0, t0 + nt) (frame-range form)
+    const float* gob = go + size_t(ti - a.d.t0) * frameF + cc;
+    const int32_t* cb = counts + size_t(ti - a.d.t0) * H * W;
 #pragma unroll
     for (int i = 0; i < P; ++i)
 #pragma unroll

@@ -448,6 +448,14 @@ int snls_replay(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const flo
 int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad,
                     const float* offsets, const float* chains, const float* q, const float* k,
                     float* dq, float* dk, float* dff, float* dbf) {
+    return snls_search_bwd_frames(ctx, cfg, dims, 0, dims.t, grad, offsets, chains, q, k, dq, dk,
+                                  dff, dbf);
+}
+
+int snls_search_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                           const float* grad, const float* offsets, const float* chains,
+                           const float* q, const float* k, float* dq, float* dk, float* dff,
+                           float* dbf) {
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = validate(cfg)) return rc;
     if (int rc = check_dims(dims)) return rc;
@@ -455,8 +463,10 @@ int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const
         return fail(SNLS_EARG, "shifted_nls_backward: null tensor");
     if (cfg->wt > 1 && !chains)
         return fail(SNLS_EARG, "shifted_nls_backward: the tape needs chains when wt > 1");
+    if (t0 < 0 || t1 > dims.t || t0 >= t1)
+        return fail(SNLS_EARG, "shifted_nls_backward: empty or invalid frame range");
     DeviceGuard g(ctx->device);
-    const Dims d = make_dims(dims, cfg->stride0);
+    const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     const size_t nv = size_t(dims.t) * dims.h * dims.w;
     cudaMemsetAsync(dq, 0, nv * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
@@ -520,13 +530,22 @@ int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
 int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad_out,
                    const int32_t* counts, const float* v, const float* weights, const float* offsets,
                    float* dv, float* dw) {
+    return snls_wpsum_bwd_frames(ctx, cfg, dims, 0, dims.t, grad_out, counts, v, weights, offsets,
+                                 dv, dw);
+}
+
+int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* grad_out, const int32_t* counts, const float* v,
+                          const float* weights, const float* offsets, float* dv, float* dw) {
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = validate(cfg)) return rc;
     if (int rc = check_dims(dims)) return rc;
     if (!grad_out || !counts || !v || !weights || !offsets || !dv || !dw)
         return fail(SNLS_EARG, "wpsum_backward: null tensor");
+    if (t0 < 0 || t1 > dims.t || t0 >= t1)
+        return fail(SNLS_EARG, "wpsum_backward: empty or invalid frame range");
     DeviceGuard g(ctx->device);
-    const Dims d = make_dims(dims, cfg->stride0);
+    const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     cudaMemsetAsync(dv, 0, size_t(dims.t) * dims.h * dims.w * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dw, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
     AggArgs a{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err};

@@ -151,6 +151,50 @@ def search_aggregate_overlapped(slab_q, slab_k, slab_v, slab_ff, slab_bf, p: Sha
     run(ib, p.b)
 
 
+def reverse_exchange_add(slab_grads, p: ShardPlan, group=None):
+    """The backward's halo step: gradients a rank accumulated into its
+    halo frames (dK / dV / dFlow land in frames qt + dt, search.cpp:584-666;
+    aggregate.cpp:412-460) belong to the owners of those frames.  Every halo range received
+    in the forward is sent back; every range sent in the forward comes back from that peer
+    as a partial sum and is added into the owned frames.  In place on the slab tensors;
+    afterwards each rank's owned frames [t0, t1) hold the full gradient."""
+    import torch
+    import torch.distributed as dist
+
+    ops, pending = [], []
+    for g in slab_grads:
+        for peer, (lo, hi), kind in transfers(p):
+            view = g[lo - p.lo:hi - p.lo]
+            if kind == "recv":  # my partial sums for the peer's frames go back to it
+                ops.append(dist.P2POp(dist.isend, view.contiguous(), peer, group))
+            else:  # the peer's partial sums for my frames
+                buf = torch.empty_like(view)
+                ops.append(dist.P2POp(dist.irecv, buf, peer, group))
+                pending.append((view, buf))
+    for r in (dist.batch_isend_irecv(ops) if ops else []):
+        r.wait()
+    for view, buf in pending:
+        view.add_(buf)
+
+
+def backward_shard(grad_sims, grad_out, res, counts, slab_q, slab_k, slab_v, p: ShardPlan, cfg,
+                   ctx=None, group=None, world=1):
+    """wpsum_backward + shifted_nls_backward for the owned rows/frames of a frame shard
+    (frame-range entry points on the slab), then the reverse halo exchange.  Returns
+    slab-shaped (dq, dk, dv, dfflow, dbflow) whose owned frames hold the full gradient
+    (Q's halo frames carry nothing: queries read only their own frame), and dweights."""
+    from . import snls as S
+
+    fr = (p.t0, p.t1)
+    dv, dw = S.wpsum_backward(grad_out, counts, slab_v, res.weights, res.offsets, cfg, ctx=ctx,
+                              check=False, frames=fr)
+    dq, dk, dff, dbf = S.shifted_nls_backward(grad_sims, res, slab_q, slab_k, ctx=ctx, check=False,
+                                              frames=fr)
+    if world > 1:
+        reverse_exchange_add([dk, dv, dff, dbf], p, group)
+    return dq, dk, dv, dff, dbf, dw
+
+
 def search_aggregate_shard(q_local, k_slab, v_slab, ff_slab, bf_slab, p: ShardPlan, cfg, ctx=None,
                            check=True):
     """Search + fused softmax + wpsum for the owned frames on the device (C-ABI frame-range

@@ -127,6 +127,8 @@ def lib() -> C.CDLL:
             L.snls_wpsum_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
                                          VOIDP, VOIDP]
             L.snls_ctx_get_stream.argtypes = [VOIDP, C.POINTER(VOIDP)]
+            L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
+            L.snls_wpsum_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7
             L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
             L.snls_host_unregister.argtypes = [VOIDP]
             L.snls_pipeline_create.argtypes = [VOIDP, P, _Dims, C.c_int, C.POINTER(VOIDP)]
@@ -368,22 +370,25 @@ def replay_similarities(res: SearchResult, q, k, ctx=None):
     return sims
 
 
-def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=True):
-    """snls::shifted_nls_backward (search.hpp:151-153) -> (dq, dk, dfflow, dbflow)."""
+def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=True, frames=None):
+    """snls::shifted_nls_backward (search.hpp:151-153) -> (dq, dk, dfflow, dbflow).
+    `frames=(t0, t1)`: the tape holds the rows of query frames [t0, t1) only (frame
+    sharding); the gradients still cover every frame of q / k."""
     import torch
 
     ctx = ctx or context(q.device.index)
     c = _cfg(res.cfg)
     t, h, w, f = q.shape
+    t0, t1 = frames if frames is not None else (0, t)
     if tuple(grad_sims.shape) != tuple(res.sims.shape):
         raise DomainError("shifted_nls_backward: gradient shape does not match the tape")
     dq = torch.empty_like(q)
     dk = torch.empty_like(q)
     dff = torch.empty((t, h, w, 2), device=q.device, dtype=torch.float32)
     dbf = torch.empty_like(dff)
-    _raise(lib().snls_search_bwd(ctx.h, C.byref(c), _dims(q), _ptr(grad_sims), _ptr(res.offsets),
-                                 _ptr(res.chains), _ptr(q), _ptr(k), _ptr(dq), _ptr(dk), _ptr(dff),
-                                 _ptr(dbf)))
+    _raise(lib().snls_search_bwd_frames(ctx.h, C.byref(c), _dims(q), int(t0), int(t1), _ptr(grad_sims),
+                                        _ptr(res.offsets), _ptr(res.chains), _ptr(q), _ptr(k),
+                                        _ptr(dq), _ptr(dk), _ptr(dff), _ptr(dbf)))
     if check:
         ctx.sync_check()
     return dq, dk, dff, dbf
@@ -452,18 +457,22 @@ def gather_stack(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True):
     return out
 
 
-def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx=None, check=True):
-    """snls::wpsum_backward (aggregate.hpp:83-85) -> (dv, dweights)."""
+def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx=None, check=True,
+                   frames=None):
+    """snls::wpsum_backward (aggregate.hpp:83-85) -> (dv, dweights).  `frames=(t0, t1)`:
+    grad_out / counts / weights / offsets hold output frames [t0, t1) only; dv covers v."""
     import torch
 
     ctx = ctx or context(v.device.index)
-    if tuple(grad_out.shape) != tuple(v.shape):
+    t0, t1 = frames if frames is not None else (0, v.shape[0])
+    if tuple(grad_out.shape) != (t1 - t0,) + tuple(v.shape[1:]):
         raise DomainError("wpsum_backward: gradient shape does not match the tape")
     c = _cfg(cfg)
     dv = torch.empty_like(v)
     dw = torch.empty_like(weights)
-    _raise(lib().snls_wpsum_bwd(ctx.h, C.byref(c), _dims(v), _ptr(grad_out), _ptr(counts), _ptr(v),
-                                _ptr(weights), _ptr(offsets), _ptr(dv), _ptr(dw)))
+    _raise(lib().snls_wpsum_bwd_frames(ctx.h, C.byref(c), _dims(v), int(t0), int(t1), _ptr(grad_out),
+                                       _ptr(counts), _ptr(v), _ptr(weights), _ptr(offsets), _ptr(dv),
+                                       _ptr(dw)))
     if check:
         ctx.sync_check()
     return dv, dw

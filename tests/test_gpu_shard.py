@@ -67,3 +67,43 @@ def test_overlapped_interior_then_edges_equals_unsharded(world):
         assert np.array_equal(host(o[3]), host(full.weights)[rows])
         assert np.array_equal(host(o[4]), host(fout)[p.a:p.b])
         assert np.array_equal(host(o[5]), host(fcnt)[p.a:p.b])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_frame_range_backward_plus_reverse_halo_equals_unsharded(world):
+    """Each rank runs wpsum_backward + shifted_nls_backward on its slab for its own rows
+    (frame-range entry points); adding every rank's slab gradients into the clip -- what
+    reverse_exchange_add does over NCCL -- gives the unsharded device gradients (fp32
+    atomics in a different order: REL_TOL)."""
+    import torch
+
+    from tests.helpers import REL_TOL, max_rel
+
+    S = snls_mod()
+    P = Checker("port")
+    T, H, W, F = 9, 18, 16, 32
+    cfg = S.SearchConfig(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2", softmax_scale=1 / 288)
+    v = dev(video(P, T, H, W, F, 31))
+    ff, bf = dev(flow(P, T, H, W, 32, 2.0)), dev(flow(P, T, H, W, 33, 2.0))
+    nq = ((H - 1) // 2 + 1) * ((W - 1) // 2 + 1)
+    gs = dev(P.uniform(34, -1, 1, T * nq * 10).reshape(T * nq, 10))
+    go = dev(P.uniform(35, -1, 1, T * H * W * F).reshape(T, H, W, F))
+    full = S.shifted_nls_forward(v, v, ff, bf, cfg, want_weights=True)
+    _, cnt = S.wpsum(v, full.weights, full.offsets, cfg)
+    want_dv, want_dw = S.wpsum_backward(go, cnt, v, full.weights, full.offsets, cfg)
+    want = S.shifted_nls_backward(gs, full, v, v)
+    acc = [torch.zeros_like(x) for x in (want[0], want[1], want_dv, want[2], want[3])]
+    for rank in range(world):
+        p = shard.plan(T, world, rank, cfg.wt)
+        sv, sff, sbf = v[p.lo:p.hi].contiguous(), ff[p.lo:p.hi].contiguous(), bf[p.lo:p.hi].contiguous()
+        res = S.shifted_nls_forward(sv, sv, sff, sbf, cfg, want_weights=True, frames=(p.t0, p.t1))
+        _, c = S.wpsum(sv, res.weights, res.offsets, cfg, frames=(p.t0, p.t1))
+        rows = slice(p.a * nq, p.b * nq)
+        out = shard.backward_shard(gs[rows].contiguous(), go[p.a:p.b].contiguous(), res, c, sv, sv, sv,
+                                   p, cfg)
+        dq, dk, dv, dff, dbf, dw = out
+        assert max_rel(host(dw), host(want_dw)[rows]) <= REL_TOL
+        for a_, g in zip(acc, (dq, dk, dv, dff, dbf)):
+            a_[p.lo:p.hi] += g
+    for a_, w in zip(acc, (want[0], want[1], want_dv, want[2], want[3])):
+        assert max_rel(host(a_), host(w)) <= REL_TOL

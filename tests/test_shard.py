@@ -157,3 +157,79 @@ def test_gloo_inplace_async_exchange(tmp_path, world, T):
     for r in range(world):
         z = np.load(tmp_path / f"a{r}.npz")
         assert np.array_equal(z["slab"], z["want"]) and np.array_equal(z["flow"], -z["want"])
+
+
+def _bwd_worker(rank, world, port, T, out_dir):
+    """Sharded backward through the oracle on each slab (owned rows only: zero upstream
+    gradient elsewhere), then the reverse halo exchange."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Cfg, Checker
+    from paper_2309_16849_b200 import shard as SH
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    P = Checker("port")
+    H = W = 10
+    F = 4
+    cfg = Cfg(ws=3, wt=2, ps=3, stride0=2, stride1=1.0, topl=3, metric="l2", softmax_scale=0.1)
+    v, ff, bf, gs, go = _bwd_inputs(P, T, H, W, F)
+    p = SH.plan(T, world, rank, cfg.wt)
+    nq = 25
+    sv, sff, sbf = v[p.lo:p.hi], ff[p.lo:p.hi], bf[p.lo:p.hi]
+    res = P.search_fwd(sv, sv, sff, sbf, cfg)
+    wts = P.softmax_rows(res["sims"], cfg.softmax_scale)
+    _, counts = P.wpsum(sv, wts, res["offsets"], cfg)
+    g_s = np.zeros_like(res["sims"])
+    g_s[p.t0 * nq:p.t1 * nq] = gs[p.a * nq:p.b * nq]
+    g_o = np.zeros_like(sv)
+    g_o[p.t0:p.t1] = go[p.a:p.b]
+    # the owned frames' counts are the unsharded counts; halo frames carry zero gradient
+    dv, _ = P.wpsum_bwd(g_o, counts, sv, wts, res["offsets"], cfg)
+    gb = P.search_bwd(sv, sv, cfg, res["centers"], res["chains"], g_s)
+    grads = [torch.tensor(x) for x in (gb["dk"], dv, gb["dfflow"], gb["dbflow"])]
+    SH.reverse_exchange_add(grads, p)
+    np.savez(os.path.join(out_dir, f"b{rank}.npz"), dq=gb["dq"][p.t0:p.t1],
+             **{n: g[p.t0:p.t1].numpy() for n, g in zip(("dk", "dv", "dff", "dbf"), grads)},
+             a=p.a, b=p.b)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _bwd_inputs(P, T, H, W, F):
+    def frame(t, seed, lo, hi, c):
+        return P.uniform(seed * 1000 + t, lo, hi, H * W * c).reshape(H, W, c)
+    f32 = lambda x: x.astype(np.float32).astype(np.float64)  # noqa: E731
+    v = f32(np.stack([frame(t, 500, -1, 1, F) for t in range(T)]))
+    ff = f32(np.stack([frame(t, 501, -1.5, 1.5, 2) for t in range(T)]))
+    bf = f32(np.stack([frame(t, 502, -1.5, 1.5, 2) for t in range(T)]))
+    gs = f32(P.uniform(503, -1, 1, T * 25 * 3).reshape(T * 25, 3))
+    go = f32(P.uniform(504, -1, 1, T * H * W * F).reshape(T, H, W, F))
+    return v, ff, bf, gs, go
+
+
+@pytest.mark.parametrize("world,T", [(2, 7), (3, 8)])
+def test_gloo_reverse_halo_backward_matches_unsharded_oracle(tmp_path, world, T):
+    import torch.multiprocessing as mp
+
+    from oracle.oracle import Cfg, Checker
+
+    mp.spawn(_bwd_worker, args=(world, _free_port(), T, str(tmp_path)), nprocs=world, join=True)
+    P = Checker("port")
+    cfg = Cfg(ws=3, wt=2, ps=3, stride0=2, stride1=1.0, topl=3, metric="l2", softmax_scale=0.1)
+    v, ff, bf, gs, go = _bwd_inputs(P, T, 10, 10, 4)
+    res = P.search_fwd(v, v, ff, bf, cfg)
+    wts = P.softmax_rows(res["sims"], cfg.softmax_scale)
+    _, counts = P.wpsum(v, wts, res["offsets"], cfg)
+    dv, _ = P.wpsum_bwd(go, counts, v, wts, res["offsets"], cfg)
+    gb = P.search_bwd(v, v, cfg, res["centers"], res["chains"], gs)
+    want = {"dq": gb["dq"], "dk": gb["dk"], "dv": dv, "dff": gb["dfflow"], "dbf": gb["dbflow"]}
+    for r in range(world):
+        z = np.load(tmp_path / f"b{r}.npz")
+        a, b = int(z["a"]), int(z["b"])
+        for n, w in want.items():  # fp64, summation order differs: tight tolerance
+            assert np.allclose(z[n], w[a:b], rtol=1e-12, atol=1e-12), n

@@ -189,6 +189,27 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                           const float* grad_out, const int32_t* counts, const float* v,
                           const float* weights, const float* offsets, float* dv, float* dweights);
 
+/* ---- frame alignment ------------------------------------------
+ * Replaces snls::estimate_flow_block_matching (flow.hpp:48-49; flow.cpp:114-175) for
+ * dims.t frame pairs at once: a[t] -> b[t] (DEVICE, T x H x W x F), flow T x H x W x 2
+ * (dy, dx) per pixel of each block; strict '<' in (dy, dx) scan order, sums in fp64. */
+int snls_block_match(snls_ctx* ctx, snls_dims dims, const float* a, const float* b, int block,
+                     int radius, float* flow);
+/* psnr (tensor.cpp:79-90) of each frame of a vs b (DEVICE); dims.t values to HOST memory. */
+int snls_psnr_frames(snls_ctx* ctx, snls_dims dims, const float* a, const float* b, double peak,
+                     double* psnr_host);
+/* add_gaussian_noise (tensor.cpp:92-99) with GaussianStream(seed) (rng.hpp:30-53), HOST
+ * buffers: out = float(in + sigma * g) with the stream's fp64 draws (bitwise). */
+int snls_gaussian_noise_f32(uint64_t seed, double sigma, int64_t n, const float* in, float* out);
+/* snls::align_frames (harness.hpp:61-62; harness.cpp:72-154) over HOST buffers:
+ * clean T x H x W x F; flow_source 0 zero, 1 provided ((T-1) x H x W x 2), 2 block
+ * matching (bm_block, bm_radius); outputs aligned (T-1) x H x W x F, top1_offsets
+ * rows x 3 (may be NULL), used_flow (T-1) x H x W x 2 (may be NULL), frame_psnr T-1. */
+int snls_align_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* clean,
+                      double sigma, uint64_t seed, int flow_source, const float* provided_flow,
+                      int bm_block, int bm_radius, float* aligned, float* top1_offsets,
+                      float* used_flow, double* frame_psnr);
+
 /* ---- host-buffer pipeline (the search -> softmax_rows -> wpsum core of align_frames /
  * run_benchmark, harness.cpp:105-154, 242-283, over HOST memory) ---------------------
  * One call copies the clip in frame by frame on a copy stream, runs search (+ fused

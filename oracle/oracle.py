@@ -296,5 +296,80 @@ class Checker:
         return dv, dw
 
 
+    # ---- frame alignment pieces (flow.cpp:114-175, tensor.cpp:79-99, harness.cpp:72-154) ----
+    def block_match(self, a, b, block: int, radius: int):
+        """a, b: single frames h x w x f -> flow h x w x 2 (estimate_flow_block_matching)."""
+        a, b = _d(a), _d(b)
+        h, w, f = a.shape
+        flow = np.zeros((h, w, 2))
+        self._check(self._fn("block_match")(h, w, f, _ptr(a), _ptr(b), block, radius, _ptr(flow)))
+        return flow
+
+    def psnr(self, a, b, peak: float = 255.0) -> float:
+        a, b = _d(a), _d(b)
+        out = C.c_double()
+        if self.which == "port":
+            self._check(self._fn("psnr")(C.c_int64(a.size), _ptr(a), _ptr(b), C.c_double(peak),
+                                         C.byref(out)))
+        else:
+            t, h, w, f = a.shape if a.ndim == 4 else (1,) + a.shape
+            self._check(self._fn("psnr")(t, h, w, f, _ptr(a), _ptr(b), C.c_double(peak), C.byref(out)))
+        return out.value
+
+    def add_gaussian_noise(self, v, sigma: float, seed: int):
+        """tensor.cpp:92-99: v + sigma * GaussianStream(seed), element order."""
+        v = _d(v)
+        if self.which == "port":
+            g = np.empty(v.size)
+            self.lib.oracle_gaussian_fill.argtypes = [C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
+            self.lib.oracle_gaussian_fill(C.c_uint64(seed), v.size, _ptr(g))
+            return v + sigma * g.reshape(v.shape) if sigma != 0.0 else v.copy()
+        out = np.empty_like(v)
+        t, h, w, f = v.shape
+        self._check(self._fn("add_gaussian_noise")(t, h, w, f, _ptr(v), C.c_double(sigma),
+                                                   C.c_uint64(seed), _ptr(out)))
+        return out
+
+    def align_frames(self, clean, cfg: Cfg, source: int = 0, provided=None, sigma: float = 0.0,
+                     seed: int = 0, bm_block: int = 9, bm_radius: int = 8, noisy=None):
+        """harness.cpp:72-154.  port: the restated pieces composed in the reference's order
+        (noise, per-pair flow, per-pair search / softmax / wpsum / psnr); `noisy` overrides
+        the noise step (e.g. fp32-rounded noisy frames).  reference: snls::align_frames."""
+        clean = _d(clean)
+        t, h, w, f = clean.shape
+        if self.which != "port":
+            nq = ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+            aligned = np.zeros((t - 1, h, w, f))
+            offs = np.zeros(((t - 1) * nq, 3))
+            used = np.zeros((t - 1, h, w, 2))
+            ps = np.zeros(t - 1)
+            prov = _d(provided) if provided is not None else np.zeros(1)
+            c = _ccfg(cfg)
+            self._check(self._fn("align_frames")(t, h, w, f, _ptr(clean), C.byref(c), source,
+                                                 _ptr(prov), C.c_double(sigma), C.c_uint64(seed),
+                                                 bm_block, bm_radius, _ptr(aligned), _ptr(offs),
+                                                 _ptr(used), _ptr(ps)))
+            return {"aligned": aligned, "offsets": offs, "used_flow": used, "psnr": ps}
+        if noisy is None:
+            noisy = self.add_gaussian_noise(clean, sigma, seed) if sigma > 0 else clean
+        used = np.zeros((t - 1, h, w, 2))
+        for ti in range(t - 1):
+            if source == 1:
+                used[ti] = provided[ti]
+            elif source == 2:
+                used[ti] = self.block_match(noisy[ti], noisy[ti + 1], bm_block, bm_radius)
+        zero_b = np.zeros((1, h, w, 2))
+        aligned, offs, ps = [], [], []
+        for ti in range(t - 1):
+            r = self.search_fwd(noisy[ti:ti + 1], noisy[ti + 1:ti + 2], used[ti:ti + 1], zero_b, cfg)
+            wts = self.softmax_rows(r["sims"], cfg.softmax_scale)
+            out, _ = self.wpsum(clean[ti + 1:ti + 2], wts, r["offsets"], cfg)
+            aligned.append(out[0])
+            offs.append(r["offsets"].reshape(-1, 3))
+            ps.append(self.psnr(out[0], clean[ti]))
+        return {"aligned": np.stack(aligned), "offsets": np.concatenate(offs), "used_flow": used,
+                "psnr": np.array(ps)}
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_LIB)

@@ -12,6 +12,9 @@
 //   snls::wpsum_backward                        aggregate.hpp:83-85 (aggregate.cpp:412-460)
 //   snls::reference::*                          reference.hpp:10-22 (reference.cpp)
 //   snls::UniformStream                         rng.hpp:12-24
+//   snls::estimate_flow_block_matching          flow.hpp:48-49 (flow.cpp:114-175)
+//   snls::psnr / add_gaussian_noise             tensor.hpp:75,79 (tensor.cpp:79-99)
+//   snls::align_frames                          harness.hpp:61-62 (harness.cpp:72-154)
 // Status codes: 0 ok, 1 ConfigError, 2 DomainError, 3 any other exception.
 #include <cstdint>
 #include <cstring>
@@ -21,6 +24,7 @@
 
 #include "snls/aggregate.hpp"
 #include "snls/flow.hpp"
+#include "snls/harness.hpp"
 #include "snls/memory.hpp"
 #include "snls/reference.hpp"
 #include "snls/rng.hpp"
@@ -343,5 +347,53 @@ int ref_wpsum_bwd(int t, int h, int w, int f, const double* grad_out, const std:
 
 void ref_memory_reset() { snls::memory::reset(); }
 std::uint64_t ref_memory_peak() { return snls::memory::peak(); }
+
+int ref_block_match(int h, int w, int f, const double* a, const double* b, int block, int radius,
+                    double* flow) {
+    return guarded([&] {
+        const snls::FlowField fl = snls::estimate_flow_block_matching(video(1, h, w, f, a),
+                                                                      video(1, h, w, f, b), block, radius);
+        std::copy(fl.data.begin(), fl.data.end(), flow);
+    });
+}
+
+int ref_psnr(int t, int h, int w, int f, const double* a, const double* b, double peak, double* out) {
+    return guarded([&] { *out = snls::psnr(video(t, h, w, f, a), video(t, h, w, f, b), peak); });
+}
+
+int ref_add_gaussian_noise(int t, int h, int w, int f, const double* v, double sigma,
+                           std::uint64_t seed, double* out) {
+    return guarded([&] {
+        const snls::VideoTensor n = snls::add_gaussian_noise(video(t, h, w, f, v), sigma, seed);
+        std::copy(n.data.begin(), n.data.end(), out);
+    });
+}
+
+// snls::align_frames with flow source 0 zero / 1 provided / 2 block matching.  Outputs:
+// aligned (t-1) x h x w x f, top1 offsets rows x 3, used flow (t-1) x h x w x 2, psnr t-1.
+int ref_align_frames(int t, int h, int w, int f, const double* clean, const RefCfg* c, int source,
+                     const double* provided, double sigma, std::uint64_t seed, int bm_block,
+                     int bm_radius, double* aligned, double* offsets, double* used_flow,
+                     double* psnr_out) {
+    return guarded([&] {
+        snls::AlignmentOptions o;
+        o.cfg = to_cfg(c);
+        o.flow_source = source == 1 ? snls::FlowSource::kProvided
+                        : source == 2 ? snls::FlowSource::kBlockMatching
+                                      : snls::FlowSource::kZero;
+        o.sigma = sigma;
+        o.seed = seed;
+        o.bm_block = bm_block;
+        o.bm_radius = bm_radius;
+        snls::FlowField pf(t - 1, h, w);
+        if (source == 1) std::copy(provided, provided + pf.data.size(), pf.data.begin());
+        const snls::AlignmentResult r = snls::align_frames(video(t, h, w, f, clean), o,
+                                                           source == 1 ? &pf : nullptr);
+        std::copy(r.aligned.data.begin(), r.aligned.data.end(), aligned);
+        std::copy(r.top1_offsets.data.begin(), r.top1_offsets.data.end(), offsets);
+        std::copy(r.used_flow.data.begin(), r.used_flow.data.end(), used_flow);
+        std::copy(r.report.frame_psnr.begin(), r.report.frame_psnr.end(), psnr_out);
+    });
+}
 
 }  // extern "C"

@@ -795,3 +795,72 @@ int oracle_wpsum_bwd(int t, int h, int w, int f, const double* grad_out, const i
         backprop_query(&s, grad_out, counts, v, weights, offsets, l, row, dv, NULL);
     return ORACLE_OK;
 }
+
+/* ---- flow.cpp:114-175 estimate_flow_block_matching ---------------------------------- */
+int oracle_block_match(int h, int w, int f, const double* a, const double* b, int block,
+                       int radius, double* flow) {
+    if (block < 1 || block % 2 == 0)
+        return fail(ORACLE_ECONFIG, "estimate_flow_block_matching: block must be odd and positive");
+    if (radius < 0) return fail(ORACLE_ECONFIG, "estimate_flow_block_matching: radius must be >= 0");
+    const int nby = (h + block - 1) / block, nbx = (w + block - 1) / block;
+    for (int bi = 0; bi < nby * nbx; ++bi) {
+        const int by = bi / nbx, bx = bi % nbx;
+        const int y0 = by * block, x0 = bx * block;
+        const int y1 = y0 + block < h ? y0 + block : h, x1 = x0 + block < w ? x0 + block : w;
+        double best = INFINITY;
+        int bdy = 0, bdx = 0;
+        for (int dy = -radius; dy <= radius; ++dy)
+            for (int dx = -radius; dx <= radius; ++dx) {
+                double ssd = 0.0;
+                for (int y = y0; y < y1; ++y) {
+                    const int ry = oracle_reflect_index(y + dy, h);
+                    for (int x = x0; x < x1; ++x) {
+                        const int rx = oracle_reflect_index(x + dx, w);
+                        for (int c = 0; c < f; ++c) {
+                            const double d = a[((int64_t)y * w + x) * f + c] - b[((int64_t)ry * w + rx) * f + c];
+                            ssd += d * d;
+                        }
+                    }
+                }
+                if (ssd < best) { /* strict: first hit in scan order wins ties */
+                    best = ssd;
+                    bdy = dy;
+                    bdx = dx;
+                }
+            }
+        for (int y = y0; y < y1; ++y)
+            for (int x = x0; x < x1; ++x) {
+                flow[((int64_t)y * w + x) * 2 + 0] = (double)bdy;
+                flow[((int64_t)y * w + x) * 2 + 1] = (double)bdx;
+            }
+    }
+    return ORACLE_OK;
+}
+
+/* ---- tensor.cpp:79-90 psnr ------------------------------------------------------------ */
+int oracle_psnr(int64_t n, const double* a, const double* b, double peak, double* out) {
+    if (!(peak > 0.0)) return fail(ORACLE_ECONFIG, "psnr: peak must be positive");
+    double sq = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double d = a[i] - b[i];
+        sq += d * d;
+    }
+    const double mse = sq / (double)n;
+    *out = mse == 0.0 ? INFINITY : 10.0 * log10(peak * peak / mse);
+    return ORACLE_OK;
+}
+
+/* ---- rng.hpp:30-53 GaussianStream ------------------------------------------------------ */
+void oracle_gaussian_fill(uint64_t seed, int64_t n, double* out) {
+    mt64 g;
+    mt64_seed(&g, seed);
+    const double kPi = 3.14159265358979323846;
+    for (int64_t i = 0; i < n; i += 2) {
+        const double u1 = ((double)(mt64_next(&g) >> 11) + 1.0) * 0x1.0p-53; /* (0,1] */
+        const double u2 = (double)(mt64_next(&g) >> 11) * 0x1.0p-53;         /* [0,1) */
+        const double r = sqrt(-2.0 * log(u1));
+        const double ang = 2.0 * kPi * u2;
+        out[i] = r * cos(ang);
+        if (i + 1 < n) out[i + 1] = r * sin(ang);
+    }
+}

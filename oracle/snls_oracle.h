@@ -76,6 +76,16 @@ int oracle_wpsum_bwd(int t, int h, int w, int f, const double* grad_out, const i
                      const double* v, int64_t rows, int l, const double* weights,
                      const double* offsets, const oracle_cfg* c, double* dv, double* dw);
 
+/* ---- frame-alignment pipeline pieces ------------------------- */
+/* flow.cpp:114-175: exhaustive block-matching SSD search, strict '<' (first hit in dy, dx
+ * scan order wins ties); a, b single frames h x w x f; flow h x w x 2 (dy, dx). */
+int oracle_block_match(int h, int w, int f, const double* a, const double* b, int block,
+                       int radius, double* flow);
+/* tensor.cpp:79-90 (inf when the inputs are identical) */
+int oracle_psnr(int64_t n, const double* a, const double* b, double peak, double* out);
+/* rng.hpp:30-53 GaussianStream(seed): n standard-normal draws (Box-Muller pairs) */
+void oracle_gaussian_fill(uint64_t seed, int64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -552,4 +552,81 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
     return after_launch(ctx, launch_wpsum_bwd(a, grad_out, counts, dv, dw, ctx->stream), "snls_wpsum_bwd");
 }
 
+// ---- frame-alignment pieces (flow.cpp:114-175, tensor.cpp:79-99) ---------------------
+int snls_block_match(snls_ctx* ctx, snls_dims dims, const float* a, const float* b, int block,
+                     int radius, float* flow) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (block < 1 || block % 2 == 0)
+        return fail(SNLS_ECONFIG, "estimate_flow_block_matching: block must be odd and positive");
+    if (radius < 0) return fail(SNLS_ECONFIG, "estimate_flow_block_matching: radius must be >= 0");
+    if (int rc = check_dims(dims)) return rc;
+    if (!a || !b || !flow) return fail(SNLS_EARG, "estimate_flow_block_matching: null tensor");
+    DeviceGuard g(ctx->device);
+    const int n = launch_block_match(a, b, dims.t, dims.h, dims.w, dims.f, block, radius, flow, ctx->stream);
+    if (n < 0) return fail(SNLS_ECONFIG, "estimate_flow_block_matching: block too large for the device");
+    return after_launch(ctx, n, "snls_block_match");
+}
+
+int snls_psnr_frames(snls_ctx* ctx, snls_dims dims, const float* a, const float* b, double peak,
+                     double* psnr_host) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (!(peak > 0.0)) return fail(SNLS_ECONFIG, "psnr: peak must be positive");
+    if (int rc = check_dims(dims)) return rc;
+    if (!a || !b || !psnr_host) return fail(SNLS_EARG, "psnr: null tensor");
+    DeviceGuard g(ctx->device);
+    const size_t nd = psnr_scratch_doubles(dims.t) + size_t(dims.t);
+    if (int rc = ensure_work(ctx, nd * sizeof(double))) return rc;
+    double* part = static_cast<double*>(ctx->work);
+    double* out = part + psnr_scratch_doubles(dims.t);
+    const int n = launch_psnr(a, b, dims.t, size_t(dims.h) * dims.w * dims.f, peak, part, out, ctx->stream);
+    if (int rc = after_launch(ctx, n, "snls_psnr_frames")) return rc;
+    cudaError_t e = cudaMemcpyAsync(psnr_host, out, size_t(dims.t) * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_psnr_frames");
+    return SNLS_OK;
+}
+
+// GaussianStream (rng.hpp:30-53) + add_gaussian_noise (tensor.cpp:92-99) on the host, fp64
+// like the reference, the result rounded to fp32.
+int snls_gaussian_noise_f32(uint64_t seed, double sigma, int64_t n, const float* in, float* out) {
+    if (sigma < 0.0) return fail(SNLS_ECONFIG, "add_gaussian_noise: sigma must be non-negative");
+    if (n > 0 && (!in || !out)) return fail(SNLS_EARG, "add_gaussian_noise: null buffer");
+    if (sigma == 0.0) {
+        if (out != in) std::memcpy(out, in, size_t(n) * sizeof(float));
+        return SNLS_OK;
+    }
+    uint64_t mt[312];
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+    int idx = 312;
+    auto next = [&]() {
+        if (idx >= 312) {
+            for (int j = 0; j < 312; ++j) {
+                const uint64_t x = (mt[j] & 0xFFFFFFFF80000000ULL) | (mt[(j + 1) % 312] & 0x7FFFFFFFULL);
+                uint64_t xa = x >> 1;
+                if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+                mt[j] = mt[(j + 156) % 312] ^ xa;
+            }
+            idx = 0;
+        }
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ULL;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+        y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+        y ^= y >> 43;
+        return y;
+    };
+    const double kPi = 3.14159265358979323846;
+    for (int64_t i = 0; i < n; i += 2) {
+        const double u1 = (double(next() >> 11) + 1.0) * 0x1.0p-53;  // (0,1]
+        const double u2 = double(next() >> 11) * 0x1.0p-53;          // [0,1)
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double ang = 2.0 * kPi * u2;
+        out[i] = float(double(in[i]) + sigma * (r * std::cos(ang)));
+        if (i + 1 < n) out[i + 1] = float(double(in[i + 1]) + sigma * (r * std::sin(ang)));
+    }
+    return SNLS_OK;
+}
+
 }  // extern "C"

@@ -65,6 +65,13 @@ int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st);
 int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                      float* dw, cudaStream_t st);
 
+// align.cu: block matching (flow.cpp:114-175) over `frames` pairs; per-frame PSNR.
+int launch_block_match(const float* a, const float* b, int frames, int h, int w, int f, int block,
+                       int radius, float* flow, cudaStream_t st);
+int launch_psnr(const float* a, const float* b, int frames, size_t n, double peak, double* part,
+                double* out, cudaStream_t st);
+size_t psnr_scratch_doubles(int frames);
+
 // `gyx`: rows * topl * 2 doubles of zeroed scratch.  Returns the number of launches.
 int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
                            const float* q, const float* k, Dims d, int wt, int ps, int topl,

@@ -127,6 +127,11 @@ def lib() -> C.CDLL:
             L.snls_wpsum_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
                                          VOIDP, VOIDP]
             L.snls_ctx_get_stream.argtypes = [VOIDP, C.POINTER(VOIDP)]
+            L.snls_block_match.argtypes = [VOIDP, _Dims, VOIDP, VOIDP, C.c_int, C.c_int, VOIDP]
+            L.snls_psnr_frames.argtypes = [VOIDP, _Dims, VOIDP, VOIDP, C.c_double, VOIDP]
+            L.snls_gaussian_noise_f32.argtypes = [C.c_uint64, C.c_double, C.c_int64, VOIDP, VOIDP]
+            L.snls_align_frames.argtypes = [VOIDP, P, _Dims, VOIDP, C.c_double, C.c_uint64, C.c_int,
+                                            VOIDP, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
             L.snls_wpsum_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7
             L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
@@ -530,3 +535,75 @@ def host_register(buf) -> None:
     ptr = buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data
     n = buf.numel() * buf.element_size() if hasattr(buf, "numel") else buf.nbytes
     _raise(lib().snls_host_register(VOIDP(ptr), n))
+
+
+# ---------------------------------------------------------------------------------------
+# frame alignment: flow.cpp:114-175, tensor.cpp:79-99, harness.cpp:72-154
+FLOW_ZERO, FLOW_PROVIDED, FLOW_BLOCK_MATCHING = 0, 1, 2
+
+
+def block_match(a, b, block: int = 9, radius: int = 8, ctx=None):
+    """estimate_flow_block_matching for every frame pair a[t] -> b[t] (torch CUDA T x H x W x F)
+    -> flow T x H x W x 2."""
+    import torch
+
+    ctx = ctx or context(a.device.index)
+    if tuple(a.shape) != tuple(b.shape):
+        raise DomainError("estimate_flow_block_matching: shape mismatch")
+    t, h, w, f = a.shape
+    flow = torch.empty((t, h, w, 2), device=a.device, dtype=torch.float32)
+    _raise(lib().snls_block_match(ctx.h, _Dims(t, h, w, f), _ptr(a), _ptr(b), int(block), int(radius),
+                                  _ptr(flow)))
+    return flow
+
+
+def psnr_frames(a, b, peak: float = 255.0, ctx=None):
+    """psnr (tensor.cpp:79-90) per frame -> list of floats."""
+    ctx = ctx or context(a.device.index)
+    if tuple(a.shape) != tuple(b.shape):
+        raise DomainError("psnr: shape mismatch")
+    t = a.shape[0]
+    out = (C.c_double * t)()
+    _raise(lib().snls_psnr_frames(ctx.h, _dims(a), _ptr(a), _ptr(b), float(peak), out))
+    return list(out)
+
+
+def add_gaussian_noise(v, sigma: float, seed: int):
+    """add_gaussian_noise (tensor.cpp:92-99) on a float32 numpy array (host)."""
+    import numpy as np
+
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    out = np.empty_like(v)
+    _raise(lib().snls_gaussian_noise_f32(C.c_uint64(seed), float(sigma), v.size, v.ctypes.data,
+                                         out.ctypes.data))
+    return out
+
+
+def align_frames(clean, cfg: SearchConfig, flow_source: int = FLOW_ZERO, provided_flow=None,
+                 sigma: float = 0.0, seed: int = 0, bm_block: int = 9, bm_radius: int = 8, ctx=None):
+    """snls::align_frames (harness.hpp:61-62) over a HOST float32 clip T x H x W x F ->
+    dict(aligned, top1_offsets, used_flow, frame_psnr, mean_psnr)."""
+    import numpy as np
+
+    ctx = ctx or context()
+    clean = np.ascontiguousarray(clean, dtype=np.float32)
+    t, h, w, f = clean.shape
+    c = _cfg(cfg)
+    pairs = max(t - 1, 0)
+    nq = ((h - 1) // cfg.stride0 + 1) * ((w - 1) // cfg.stride0 + 1)
+    aligned = np.zeros((pairs, h, w, f), np.float32)
+    offs = np.zeros((pairs * nq, 3), np.float32)
+    used = np.zeros((pairs, h, w, 2), np.float32)
+    ps = np.zeros(pairs, np.float64)
+    prov = None
+    if provided_flow is not None:
+        prov = np.ascontiguousarray(provided_flow, dtype=np.float32)
+        if prov.shape[1:3] != (h, w) or prov.shape[0] < pairs:
+            raise DomainError("align_frames: provided flow does not cover every frame pair")
+    _raise(lib().snls_align_frames(ctx.h, C.byref(c), _Dims(t, h, w, f), clean.ctypes.data,
+                                   float(sigma), C.c_uint64(seed), int(flow_source),
+                                   None if prov is None else prov.ctypes.data, int(bm_block),
+                                   int(bm_radius), aligned.ctypes.data, offs.ctypes.data,
+                                   used.ctypes.data, ps.ctypes.data))
+    return {"aligned": aligned, "top1_offsets": offs, "used_flow": used, "frame_psnr": ps,
+            "mean_psnr": float(ps.mean()) if pairs else float("nan")}

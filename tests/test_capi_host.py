@@ -88,3 +88,20 @@ def test_null_arguments_rejected_before_any_device_work(S):
     lib.snls_last_error.restype = C.c_char_p
     assert lib.snls_search_fwd(None, None, S._Dims(1, 1, 1, 1), None, None, None, None, 0,
                                None, None, None, None) == 4
+
+
+def test_host_gaussian_noise_matches_reference_stream():
+    """snls_gaussian_noise_f32 (host side of align_frames) == add_gaussian_noise with the
+    reference's GaussianStream (rng.hpp:30-53), rounded to fp32 -- no device needed."""
+    import numpy as np
+
+    from oracle.oracle import Checker
+    from paper_2309_16849_b200 import snls as S
+
+    P = Checker("port")
+    v = np.floor(P.uniform(3, 0, 256, 2 * 6 * 5 * 3)).reshape(2, 6, 5, 3).astype(np.float32)
+    for sigma, seed in ((0.0, 1), (4.0, 2), (30.0, 99)):
+        want = P.add_gaussian_noise(v.astype(np.float64), sigma, seed).astype(np.float32)
+        assert np.array_equal(S.add_gaussian_noise(v, sigma, seed), want)
+    with pytest.raises(S.ConfigError, match="sigma must be non-negative"):
+        S.add_gaussian_noise(v, -1.0, 0)

@@ -1,0 +1,112 @@
+"""GPU parity of the frame-alignment pipeline around the search:
+block-matching flow (flow.cpp:114-175) bit-exact against the oracle on fp32-representable
+frames (fp64 sums in the reference's order, same tie rule), per-frame PSNR, and
+align_frames end to end -- against the oracle's composition of the restated pieces on the
+same fp32 noisy clip, and against the reference's own align_frames where the arithmetic is
+exact (noise-free 8-bit clips)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Cfg, Checker, have_reference
+from tests.gpu_util import dev, host, snls_mod
+from tests.helpers import REL_TOL, max_rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(P, t, h, w, f, seed, integer=True):
+    v = P.uniform(seed, 0, 256, t * h * w * f).reshape(t, h, w, f)
+    return np.floor(v) if integer else v.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("block,radius,integer", [(9, 8, True), (5, 3, False), (3, 1, True), (7, 0, False)])
+def test_block_match_bit_exact(block, radius, integer):
+    S = snls_mod()
+    P = Checker("port")
+    t, h, w, f = 3, 37, 29, 3
+    a = _frames(P, t, h, w, f, 11, integer)
+    b = np.roll(a, (2, -3), axis=(1, 2))
+    b[1] = _frames(P, 1, h, w, f, 12, integer)[0]  # one unrelated pair
+    got = host(S.block_match(dev(a), dev(b), block, radius))
+    for ti in range(t):
+        assert np.array_equal(got[ti], P.block_match(a[ti], b[ti], block, radius)), ti
+    with pytest.raises(S.ConfigError, match="block must be odd and positive"):
+        S.block_match(dev(a), dev(b), 4, 1)
+
+
+def test_psnr_frames():
+    S = snls_mod()
+    P = Checker("port")
+    a = _frames(P, 4, 20, 18, 3, 21, False)
+    b = a + P.uniform(22, -3, 3, a.size).reshape(a.shape).astype(np.float32)
+    b = b.astype(np.float32).astype(np.float64)
+    got = S.psnr_frames(dev(a), dev(b))
+    for ti in range(4):
+        assert abs(got[ti] - P.psnr(a[ti], b[ti])) <= 1e-12 * abs(P.psnr(a[ti], b[ti]))
+    assert S.psnr_frames(dev(a), dev(a)) == [np.inf] * 4
+
+
+def test_gaussian_noise_is_the_reference_stream():
+    S = snls_mod()
+    P = Checker("port")
+    v = _frames(P, 2, 9, 7, 3, 31, True).astype(np.float32)
+    want = P.add_gaussian_noise(v.astype(np.float64), 12.5, 77).astype(np.float32)
+    assert np.array_equal(S.add_gaussian_noise(v, 12.5, 77), want)
+
+
+@pytest.mark.parametrize("source", [0, 2])
+def test_align_frames_vs_oracle_composition(source):
+    S = snls_mod()
+    P = Checker("port")
+    t, h, w, f = 4, 30, 26, 3
+    clean = _frames(P, t, h, w, f, 41, True)
+    cfg = Cfg(ws=7, wt=1, ps=3, stride0=2, topl=1, metric="l2", softmax_scale=1.0)
+    scfg = S.SearchConfig(**cfg.__dict__)
+    r = S.align_frames(clean, scfg, flow_source=source, sigma=10.0, seed=5, bm_block=5, bm_radius=3)
+    noisy = S.add_gaussian_noise(clean.astype(np.float32), 10.0, 5).astype(np.float64)
+    want = P.align_frames(clean, cfg, source=source, bm_block=5, bm_radius=3, noisy=noisy)
+    assert np.array_equal(r["used_flow"], want["used_flow"])
+    # selection: equal except rows whose oracle top-2 gap is a (near-)tie -- incl. exact fp64
+    # ties of reflected permutations (gradcheck_util.hpp:61-69)
+    nq = want["offsets"].shape[0] // (t - 1)
+    zb = np.zeros((1, h, w, 2))
+    c2 = Cfg(**{**cfg.__dict__, "topl": 2})
+    near = np.concatenate([
+        (lambda s2: (s2[:, 0] - s2[:, 1]) < 1e-4 * np.maximum(1, np.abs(s2[:, 0])))(
+            P.search_fwd(noisy[ti:ti + 1], noisy[ti + 1:ti + 2], want["used_flow"][ti:ti + 1], zb, c2)["sims"])
+        for ti in range(t - 1)])
+    same = np.all(r["top1_offsets"] == want["offsets"], axis=1)
+    assert np.all(same | near), np.argwhere(~(same | near))[:5]
+    # aggregation + PSNR of the device's own selection (top-1 weight is exactly 1)
+    for ti in range(t - 1):
+        o = r["top1_offsets"][ti * nq:(ti + 1) * nq].astype(np.float64).reshape(nq, 1, 3)
+        agg, _ = P.wpsum(clean[ti + 1:ti + 2], np.ones((nq, 1)), o, cfg)
+        assert max_rel(r["aligned"][ti], agg[0]) <= REL_TOL
+        assert abs(r["frame_psnr"][ti] - P.psnr(agg[0], clean[ti])) <= 1e-9 * abs(r["frame_psnr"][ti])
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built")
+def test_align_frames_exact_against_reference():
+    """Noise-free 8-bit clip, block-matching flow: every sum is exact in fp32, the top-1
+    weight is 1 -- the device pipeline reproduces snls::align_frames itself."""
+    S = snls_mod()
+    P, R = Checker("port"), Checker("reference")
+    t, h, w, f = 4, 24, 22, 3
+    clean = _frames(P, t, h, w, f, 51, True)
+    clean[1:] = np.roll(clean[:-1], (1, 2), axis=(1, 2))  # a moving clip
+    cfg = Cfg(ws=5, wt=0, ps=1, stride0=1, topl=1, metric="l2", softmax_scale=1.0)
+    r = S.align_frames(clean, S.SearchConfig(**cfg.__dict__), flow_source=2, bm_block=5, bm_radius=2)
+    want = R.align_frames(clean, cfg, source=2, bm_block=5, bm_radius=2)
+    assert np.array_equal(r["used_flow"], want["used_flow"])
+    assert np.array_equal(r["top1_offsets"], want["offsets"])
+    assert np.array_equal(r["aligned"], want["aligned"])
+    assert np.allclose(r["frame_psnr"], want["psnr"], rtol=1e-12)
+
+
+def test_align_frames_errors():
+    S = snls_mod()
+    clean = np.zeros((3, 8, 8, 1), np.float32)
+    with pytest.raises(S.ConfigError, match="align_frames: requires topl == 1"):
+        S.align_frames(clean, S.SearchConfig(ws=3, ps=1, topl=2))
+    with pytest.raises(S.DomainError, match="align_frames: needs at least two frames"):
+        S.align_frames(clean[:1], S.SearchConfig(ws=3, ps=1, topl=1))

@@ -145,3 +145,54 @@ def test_underfull_and_hole_errors(port):
     v = video(port, 1, 6, 6, 1, 71)
     with pytest.raises(OracleError, match="hole-free"):
         port.wpsum(v, np.ones((36, 1)), np.zeros((36, 1, 3)), Cfg(ws=3, ps=3, stride0=1, topl=1))
+
+
+# ---- frame-alignment pieces: the restatement vs the reference -----
+def _ref():
+    from oracle.oracle import Checker, have_reference
+
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    return Checker("reference")
+
+
+def test_block_match_port_equals_reference():
+    from oracle.oracle import Checker
+
+    P, R = Checker("port"), _ref()
+    rng = np.random.default_rng(5)
+    for i in range(6):
+        h, w, f = int(rng.integers(5, 23)), int(rng.integers(5, 23)), int(rng.choice([1, 3]))
+        block, radius = int(rng.choice([1, 3, 5, 9])), int(rng.integers(0, 5))
+        a = np.floor(P.uniform(700 + i, 0, 256, h * w * f)).reshape(h, w, f)
+        b = np.roll(a, (1, -2), axis=(0, 1)) if i % 2 else np.floor(P.uniform(800 + i, 0, 256, h * w * f)).reshape(h, w, f)
+        assert np.array_equal(P.block_match(a, b, block, radius), R.block_match(a, b, block, radius))
+    with pytest.raises(Exception, match="block must be odd"):
+        P.block_match(np.zeros((4, 4, 1)), np.zeros((4, 4, 1)), 2, 1)
+
+
+def test_psnr_and_gaussian_noise_port_equal_reference():
+    from oracle.oracle import Checker
+
+    P, R = Checker("port"), _ref()
+    v = P.uniform(31, 0, 255, 2 * 5 * 7 * 3).reshape(2, 5, 7, 3)
+    for sigma, seed in ((0.0, 1), (10.0, 7), (25.0, 123)):
+        assert np.array_equal(P.add_gaussian_noise(v, sigma, seed), R.add_gaussian_noise(v, sigma, seed))
+    n = R.add_gaussian_noise(v, 15.0, 3)
+    assert P.psnr(n, v) == R.psnr(n, v)
+    assert P.psnr(v, v) == np.inf
+
+
+@pytest.mark.parametrize("source", [0, 2])
+def test_align_frames_composition_equals_reference(source):
+    """The oracle's composition of the restated pieces reproduces snls::align_frames."""
+    from oracle.oracle import Cfg, Checker
+
+    P, R = Checker("port"), _ref()
+    t, h, w, f = 3, 14, 12, 3
+    clean = np.floor(P.uniform(41, 0, 256, t * h * w * f)).reshape(t, h, w, f)
+    cfg = Cfg(ws=5, wt=0, ps=3, stride0=2, stride1=1.0, topl=1, metric="l2", softmax_scale=1.0)
+    a = P.align_frames(clean, cfg, source=source, sigma=8.0, seed=9, bm_block=5, bm_radius=2)
+    b = R.align_frames(clean, cfg, source=source, sigma=8.0, seed=9, bm_block=5, bm_radius=2)
+    for k in ("aligned", "offsets", "used_flow", "psnr"):
+        assert np.array_equal(a[k], b[k]), k

@@ -320,7 +320,7 @@ def run_ours(args, wl):
     if use_pipe:
         # the C-ABI host-buffer call (snls_pipeline_run): frame-chunked kernels overlapped
         # with the H2D input / D2H result copies; Q = K = V is one host buffer, copied once
-        chunk = args.pipe_chunk or max(1, wl["T"] // 10)
+        chunk = args.pipe_chunk or 1
         pipe = S.Pipeline(cfg, vid_h.shape, chunk_frames=chunk, ctx=ctx)
 
         def e2e_step():
@@ -545,7 +545,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-crop", type=int, default=96)
     ap.add_argument("--pipe-chunk", type=int, default=int(os.environ.get("SNLS_PIPE_CHUNK", "0")),
-                    help="query frames per chunk of the e2e host pipeline (0: T/10)")
+                    help="query frames per chunk of the e2e host pipeline (0: 1)")
     ap.add_argument("--search-kernel", default=os.environ.get("SNLS_SEARCH_KERNEL", "auto"),
                     choices=["auto", "tiled", "stream"], help="stride1 == 1 register plan")
     args = ap.parse_args()

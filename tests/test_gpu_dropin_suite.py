@@ -1,0 +1,67 @@
+"""The reference's OWN unit tests (tests/test_{search,aggregate,gradcheck,harness}.cpp,
+45 test cases, ~16k checks) compiled unchanged with our doctest-compatible shim
+(paper_2309_16849_b200/host/doctest_shim) and linked two ways by host/Makefile:
+
+* suite_ref/  -- against the reference's own search.cpp / aggregate.cpp: every check passes
+  (CPU, `-m "not gpu"`): the shim runs the suite faithfully.
+* suite_gpu/  -- against the B200 drop-in adapter (the GPU kernels behind the reference API).
+  The suite was written for an fp64 implementation; every failing check must be one of:
+    - a numeric comparison (Approx with a 1e-12/1e-14 epsilon, or exact ==) whose values
+      agree to the north star's fp32 tolerance rel <= 1e-5 (gradcheck_util.hpp:19-21 metric);
+    - a listed check whose premise is fp64-only (below, each with its reason).
+  Anything else -- a wrong index, a missing exception, a wrong shape -- fails this test.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "paper_2309_16849_b200", "host", "build")
+SUITE = ["test_search", "test_aggregate", "test_gradcheck", "test_harness"]
+
+# checks whose premise only holds in fp64, with the reason
+FP64_ONLY = {
+    "test_search.cpp:345": "fused GPU result bitwise == the reference's fp64 serial twin",
+    "test_harness.cpp:63": "PSNR of an identity alignment of a random fp64 clip is inf only "
+                           "if the aligned frame is bit-identical in fp64",
+    "test_harness.cpp:64": "same, mean PSNR",
+    "test_gradcheck.cpp:74": "central finite differences with h = 1e-6 (gradcheck_util.hpp:110) "
+                             "of an fp32 forward: the FD quotient is below fp32 resolution",
+    "test_gradcheck.cpp:136": "same (flow-composition chain FD)",
+    "test_gradcheck.cpp:194": "same (wpsum FD, gradcheck_util.hpp:182)",
+}
+
+
+def _run(kind, name):
+    exe = os.path.join(BUILD, kind, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (make -C paper_2309_16849_b200/host suite)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    summary = [l for l in p.stdout.splitlines() if l.startswith("SUMMARY")]
+    assert summary, p.stdout[-2000:] + p.stderr[-2000:]
+    return [l for l in p.stdout.splitlines() if l.startswith("FAIL")], summary[0]
+
+
+@pytest.mark.parametrize("name", SUITE)
+def test_reference_suite_passes_on_reference(name):
+    fails, summary = _run("suite_ref", name)
+    assert not fails, "\n".join(fails[:20])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SUITE)
+def test_reference_suite_on_gpu_adapter(name):
+    fails, summary = _run("suite_gpu", name)
+    bad = []
+    for line in fails:
+        where = os.path.basename(line.split()[1])
+        m = re.search(r"rel=([0-9.eE+-]+|inf|nan)", line)
+        if where in FP64_ONLY:
+            continue
+        if m and float(m.group(1)) <= 1e-5:
+            continue
+        bad.append(line)
+    print(summary, f"(failures within fp32 tolerance or fp64-only premise: {len(fails) - len(bad)})")
+    assert not bad, "\n".join(bad[:20])

@@ -219,3 +219,39 @@ def test_errors_match_reference_contract(port):
         S.shifted_nls_forward(q, q, dev(bad), ff, S.SearchConfig(ws=3, ps=1, topl=1))
     with pytest.raises(S.DomainError, match="flow shape"):
         S.shifted_nls_forward(q, q, dev(np.zeros((2, 6, 5, 2))), ff, S.SearchConfig(ws=3))
+
+
+@pytest.mark.parametrize("plan", ["tiled", "stream", "generic"])
+def test_degenerate_shapes_and_far_flows(port, plan):
+    """Edge cases the reference's reflect/shift code handles (tensor.cpp:23-29 period-2(n-1)
+    mirror for ANY magnitude, n == 1 -> 0; search.cpp:72-122): 1-pixel frames, frames
+    smaller than the window, stride0 beyond the frame, flows far outside the frame (many
+    reflection folds), through every search plan, against the oracle."""
+    S = snls_mod()
+    cases = [  # (t, h, w, f, ws, wt, ps, s0, topl, flow magnitude)
+        (2, 1, 1, 4, 3, 1, 1, 1, 2, 0.7),
+        (3, 1, 7, 4, 5, 1, 3, 2, 3, 3.0),
+        (2, 5, 4, 32, 11, 1, 3, 9, 4, 60.0),
+        (4, 9, 11, 32, 11, 3, 3, 2, 16, 200.0),
+        (3, 12, 10, 64, 9, 2, 7, 4, 10, 37.5),
+        (2, 3, 3, 64, 9, 1, 3, 1, 5, 1e3),
+    ]
+    ctx = S.context()
+    for i, (t, h, w, f, ws, wt, ps, s0, topl, mag) in enumerate(cases):
+        cfg = Cfg(ws=ws, wt=wt, ps=ps, stride0=s0, topl=topl, metric="l2" if i % 2 else "ip",
+                  softmax_scale=0.01)
+        q, k = video(port, t, h, w, f, 910 + i), video(port, t, h, w, f, 920 + i)
+        ff, bf = flow(port, t, h, w, 930 + i, mag), flow(port, t, h, w, 940 + i, mag)
+        ref = port.search_fwd(q, k, ff, bf, cfg)
+        lp1 = None
+        if topl < cfg.window_slots():
+            try:
+                lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": topl + 1}))["sims"]
+            except Exception:
+                lp1 = None
+        ctx.set_search_kernel("stream" if plan == "stream" else "tiled")
+        try:
+            r = gpu_search(q, k, ff, bf, cfg, generic=plan == "generic")
+        finally:
+            ctx.set_search_kernel("auto")
+        compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)

@@ -46,7 +46,9 @@ __device__ __forceinline__ void lerpv(float (&r)[VEC], const float (&a)[VEC], co
     for (int v = 0; v < VEC; ++v) r[v] = fmaf(w11, d[v], fmaf(w10, c[v], fmaf(w01, b[v], w00 * a[v])));
 }
 
-template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB>
+// QREG: the query patch (P x P x VEC per lane) is loaded once into registers instead of
+// being re-read from L1 on every region row (used where it fits: ps = 7 on float2 lanes).
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
     constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
@@ -72,6 +74,14 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     for (int p = 0; p < P; ++p) {
         qrow[p] = reflect_near(qy + p - HP, H) * Wd * F;
         qcol[p] = reflect_near(qx + p - HP, Wd) * F;
+    }
+
+    float qreg[QREG ? P : 1][QREG ? P : 1][VEC];
+    if constexpr (QREG) {
+#pragma unroll
+        for (int py = 0; py < P; ++py)
+#pragma unroll
+            for (int px = 0; px < P; ++px) ldv<VEC>(qbase + qrow[py] + qcol[px], qreg[py][px]);
     }
 
     TopL<W, G, KMAX> sel;
@@ -160,7 +170,12 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
 #pragma unroll
                 for (int px = 0; px < P; ++px) {
                     float qv[VEC];
-                    ldv<VEC>(qr + qcol[px], qv);
+                    if constexpr (QREG) {
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) qv[v] = qreg[P - 1 - s][px][v];
+                    } else {
+                        ldv<VEC>(qr + qcol[px], qv);
+                    }
 #pragma unroll
                     for (int b = 0; b < W; ++b)
 #pragma unroll
@@ -194,10 +209,11 @@ template <int P, int W, int VEC, int G, int KMAX, int MINB>
 int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     using C = TiledCfg<P, W, VEC, G>;
     const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
+    constexpr bool QREG = P >= 7;  // c2: 0.477 -> 0.440 ms (profiles/r01_plans.txt)
     if (s.metric == SNLS_METRIC_IP)
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG><<<blocks, 32 * C::WARPS, 0, st>>>(s);
     else
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG><<<blocks, 32 * C::WARPS, 0, st>>>(s);
     return 1;
 }
 

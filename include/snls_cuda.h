@@ -41,7 +41,8 @@ typedef enum {
     SNLS_ECONFIG = 1, /* snls::ConfigError (errors.hpp:9-12) */
     SNLS_EDOMAIN = 2, /* snls::DomainError (errors.hpp:14-17) */
     SNLS_ECUDA = 3,   /* CUDA runtime failure, no device, or the kernels are not loadable */
-    SNLS_EARG = 4     /* null or inconsistent argument at the C boundary */
+    SNLS_EARG = 4,    /* null or inconsistent argument at the C boundary */
+    SNLS_EIO = 5      /* snls::IoError (errors.hpp): file formats */
 } snls_status;
 
 typedef enum { SNLS_METRIC_IP = 0, SNLS_METRIC_L2 = 1 } snls_metric; /* search.hpp:12 */
@@ -209,6 +210,15 @@ int snls_align_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
                       double sigma, uint64_t seed, int flow_source, const float* provided_flow,
                       int bm_block, int bm_radius, float* aligned, float* top1_offsets,
                       float* used_flow, double* frame_psnr);
+
+/* ---- on-disk formats, host only ---------------------------------
+ * .stnt raw tensors (load_raw / save_raw, video_io.cpp:52-117) and Middlebury .flo
+ * (read_flo / write_flo, flow.cpp:53-112), same checks and messages (IoError -> SNLS_EIO). */
+int snls_raw_info(const char* path, snls_dims* dims, int* elem_width);
+int snls_raw_read(const char* path, float* out, int64_t capacity);      /* t*h*w*f floats */
+int snls_raw_write(const char* path, snls_dims dims, const float* data, int elem_width);
+int snls_flo_read(const char* path, int* h, int* w, float* flow_or_null); /* h x w x (dy, dx) */
+int snls_flo_write(const char* path, int h, int w, const float* flow);
 
 /* ---- host-buffer pipeline (the search -> softmax_rows -> wpsum core of align_frames /
  * run_benchmark, harness.cpp:105-154, 242-283, over HOST memory) ---------------------

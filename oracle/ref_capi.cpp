@@ -396,4 +396,20 @@ int ref_align_frames(int t, int h, int w, int f, const double* clean, const RefC
     });
 }
 
+int ref_write_flo(int h, int w, const double* flow, const char* path) {
+    return guarded([&] {
+        snls::FlowField f(1, h, w);
+        std::copy(flow, flow + f.data.size(), f.data.begin());
+        snls::write_flo(f, path);
+    });
+}
+
+int ref_read_flo(const char* path, int h, int w, double* flow) {
+    return guarded([&] {
+        const snls::FlowField f = snls::read_flo(path);
+        if (f.h != h || f.w != w) throw snls::DomainError("ref_read_flo: unexpected shape");
+        std::copy(f.data.begin(), f.data.end(), flow);
+    });
+}
+
 }  // extern "C"

@@ -39,6 +39,10 @@ class CudaError(SnlsError):
     pass
 
 
+class IoError(SnlsError):
+    """snls::IoError (errors.hpp): file formats."""
+
+
 @dataclass
 class SearchConfig:
     """snls::SearchConfig (search.hpp:17-35)."""
@@ -127,6 +131,11 @@ def lib() -> C.CDLL:
             L.snls_wpsum_bwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, VOIDP,
                                          VOIDP, VOIDP]
             L.snls_ctx_get_stream.argtypes = [VOIDP, C.POINTER(VOIDP)]
+            L.snls_raw_info.argtypes = [C.c_char_p, C.POINTER(_Dims), C.POINTER(C.c_int)]
+            L.snls_raw_read.argtypes = [C.c_char_p, VOIDP, C.c_int64]
+            L.snls_raw_write.argtypes = [C.c_char_p, _Dims, VOIDP, C.c_int]
+            L.snls_flo_read.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), VOIDP]
+            L.snls_flo_write.argtypes = [C.c_char_p, C.c_int, C.c_int, VOIDP]
             L.snls_block_match.argtypes = [VOIDP, _Dims, VOIDP, VOIDP, C.c_int, C.c_int, VOIDP]
             L.snls_psnr_frames.argtypes = [VOIDP, _Dims, VOIDP, VOIDP, C.c_double, VOIDP]
             L.snls_gaussian_noise_f32.argtypes = [C.c_uint64, C.c_double, C.c_int64, VOIDP, VOIDP]
@@ -153,6 +162,8 @@ def _raise(rc: int):
         raise DomainError(msg)
     if rc == 3:
         raise CudaError(msg)
+    if rc == 5:
+        raise IoError(msg)
     raise SnlsError(msg)
 
 
@@ -607,3 +618,43 @@ def align_frames(clean, cfg: SearchConfig, flow_source: int = FLOW_ZERO, provide
                                    used.ctypes.data, ps.ctypes.data))
     return {"aligned": aligned, "top1_offsets": offs, "used_flow": used, "frame_psnr": ps,
             "mean_psnr": float(ps.mean()) if pairs else float("nan")}
+
+
+# ---------------------------------------------------------------------------------------
+# on-disk formats: .stnt (video_io.cpp:52-117), .flo (flow.cpp:53-112)
+def read_raw(path: str):
+    """load_raw -> float32 numpy T x H x W x F (and the file's element width)."""
+    import numpy as np
+
+    d, wd = _Dims(), C.c_int()
+    _raise(lib().snls_raw_info(path.encode(), C.byref(d), C.byref(wd)))
+    out = np.empty((d.t, d.h, d.w, d.f), np.float32)
+    _raise(lib().snls_raw_read(path.encode(), out.ctypes.data, out.size))
+    return out
+
+
+def write_raw(path: str, v, width: int = 4) -> None:
+    """save_raw from a float32 array T x H x W x F (width 4: f32 payload, 8: f64)."""
+    import numpy as np
+
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    _raise(lib().snls_raw_write(path.encode(), _Dims(*v.shape), v.ctypes.data, int(width)))
+
+
+def read_flo(path: str):
+    """read_flo -> float32 numpy H x W x 2 holding (dy, dx)."""
+    import numpy as np
+
+    h, w = C.c_int(), C.c_int()
+    _raise(lib().snls_flo_read(path.encode(), C.byref(h), C.byref(w), None))
+    out = np.empty((h.value, w.value, 2), np.float32)
+    _raise(lib().snls_flo_read(path.encode(), C.byref(h), C.byref(w), out.ctypes.data))
+    return out
+
+
+def write_flo(path: str, flow) -> None:
+    """write_flo of one H x W x 2 (dy, dx) field."""
+    import numpy as np
+
+    flow = np.ascontiguousarray(flow, dtype=np.float32)
+    _raise(lib().snls_flo_write(path.encode(), flow.shape[0], flow.shape[1], flow.ctypes.data))

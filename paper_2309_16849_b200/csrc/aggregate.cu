@@ -380,7 +380,10 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 // patches of its contributing units in the reference's fixed order (footprint py, px
 // ascending, then the owning query's cell completion; aggregate.cpp:156-188), divides by the
 // count and writes once.  Deterministic, no atomics, one barrier.
-template <int P, int G, int TY, int TX>
+// FG = F / 4 float4 per pixel; a CTA covers G of them (channel slice blockIdx.y), so wide
+// videos (F = 64) split their channels over two CTAs and keep the parked patches, and the
+// shared memory per CTA, at the F = 32 size (two resident CTAs per SM instead of one).
+template <int P, int G, int FG, int TY, int TX>
 __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
                                                           int32_t* __restrict__ counts) {
     extern __shared__ float4 s_patch[];  // [query][P*P][G]
@@ -395,8 +398,9 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
     const int gx_lo = tx0 / st, gx_hi = min(a.d.nw - 1, (tx0 + TX - 1 + st - 1) / st);
     const int nqx = gx_hi - gx_lo + 1, nq = (gy_hi - gy_lo + 1) * nqx;
     const int grp = threadIdx.x / G, gl = threadIdx.x % G;
-    const unsigned row4 = unsigned(W) * G;
-    const float4* vbase = reinterpret_cast<const float4*>(a.v) + gl;
+    const unsigned row4 = unsigned(W) * FG;
+    const int cg0 = int(blockIdx.y) * G;  // first float4 channel group of this CTA
+    const float4* vbase = reinterpret_cast<const float4*>(a.v) + cg0 + gl;
 
     for (int qi = grp; qi < nq; qi += NQG) {
         const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
@@ -426,18 +430,18 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
             const float4* vf = vbase + size_t(kt) * H * row4;
             float4 blk[P + 1][P + 1];
             if (by >= 0 && by + P < H && bx >= 0 && bx + P < W) {
-                const float4* p0 = vf + (unsigned(by) * row4 + unsigned(bx) * G);
+                const float4* p0 = vf + (unsigned(by) * row4 + unsigned(bx) * FG);
 #pragma unroll
                 for (int i = 0; i <= P; ++i)
 #pragma unroll
-                    for (int j = 0; j <= P; ++j) blk[i][j] = __ldg(p0 + i * row4 + j * G);
+                    for (int j = 0; j <= P; ++j) blk[i][j] = __ldg(p0 + i * row4 + j * FG);
             } else {  // reflected border taps (tensor.cpp:31-48)
 #pragma unroll
                 for (int i = 0; i <= P; ++i) {
                     const unsigned r = unsigned(reflect_near(by + i, H)) * row4;
 #pragma unroll
                     for (int j = 0; j <= P; ++j)
-                        blk[i][j] = __ldg(vf + (r + unsigned(reflect_near(bx + j, W)) * G));
+                        blk[i][j] = __ldg(vf + (r + unsigned(reflect_near(bx + j, W)) * FG));
                 }
             }
 #pragma unroll
@@ -493,12 +497,12 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
             continue;
         }
         const float fc = float(cnt);
-        reinterpret_cast<float4*>(out + gp * a.d.f)[c] = make_float4(sum.x / fc, sum.y / fc, sum.z / fc, sum.w / fc);
-        if (c == 0 && counts) counts[gp] = cnt;
+        reinterpret_cast<float4*>(out + gp * a.d.f)[cg0 + c] = make_float4(sum.x / fc, sum.y / fc, sum.z / fc, sum.w / fc);
+        if (c == 0 && cg0 == 0 && counts) counts[gp] = cnt;
     }
 }
 
-template <int P, int G>
+template <int P, int G, int FG>
 int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     constexpr int TY = 16, TX = 16;
     const int s0 = a.d.stride0;
@@ -508,10 +512,11 @@ int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream
     const int nq = nqy * nqx;
     const size_t smem = size_t(nq) * P * P * G * sizeof(float4);
     if (smem > 200 * 1024) return 0;
-    cudaFuncSetAttribute(wpsum_query_kernel<P, G, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(wpsum_query_kernel<P, G, FG, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
     const int tiles = ((a.d.w + TX - 1) / TX) * ((a.d.h + TY - 1) / TY);
-    wpsum_query_kernel<P, G, TY, TX><<<unsigned(int64_t(a.d.nt) * tiles), 256, smem, st>>>(a, out, counts);
+    const dim3 grid(unsigned(int64_t(a.d.nt) * tiles), FG / G);
+    wpsum_query_kernel<P, G, FG, TY, TX><<<grid, 256, smem, st>>>(a, out, counts);
     return 1;
 }
 
@@ -521,16 +526,18 @@ int launch_wpsum_query_any(const AggArgs& a, float* out, int32_t* counts, cudaSt
         return e && std::atoi(e) == 1;
     }();
     if (off || a.d.f % 4 != 0) return 0;
-    const int G = a.d.f / 4;
+    const int FG = a.d.f / 4;
+    // channel slices of 8 float4 (128 B per pixel): slices of 4 measured slower (c4 0.54 ->
+    // 0.71 ms, c5 19.0 -> 25.2 ms), one 16-wide slice holds 1 CTA/SM (c5 27.3 ms)
     if (a.ps == 3) {
-        if (G == 8) return launch_wpsum_query<3, 8>(a, out, counts, st);
-        if (G == 16) return launch_wpsum_query<3, 16>(a, out, counts, st);
-        if (G == 4) return launch_wpsum_query<3, 4>(a, out, counts, st);
-        if (G == 2) return launch_wpsum_query<3, 2>(a, out, counts, st);
+        if (FG == 8) return launch_wpsum_query<3, 8, 8>(a, out, counts, st);
+        if (FG == 16) return launch_wpsum_query<3, 8, 16>(a, out, counts, st);  // two channel slices
+        if (FG == 4) return launch_wpsum_query<3, 4, 4>(a, out, counts, st);
+        if (FG == 2) return launch_wpsum_query<3, 2, 2>(a, out, counts, st);
     }
     if (a.ps == 1) {
-        if (G == 8) return launch_wpsum_query<1, 8>(a, out, counts, st);
-        if (G == 16) return launch_wpsum_query<1, 16>(a, out, counts, st);
+        if (FG == 8) return launch_wpsum_query<1, 8, 8>(a, out, counts, st);
+        if (FG == 16) return launch_wpsum_query<1, 8, 16>(a, out, counts, st);
     }
     return 0;
 }

@@ -61,3 +61,19 @@ def test_register_plan_vs_oracle(port, kernel, path, name, t, h, w, f, cfg):
         assert np.array_equal(host(again.offsets), host(r.offsets))
     finally:
         ctx.set_search_kernel("auto")
+
+
+@pytest.mark.parametrize("name,t,h,w,f,cfg", SHAPES, ids=[s[0] for s in SHAPES])
+def test_wpsum_at_baseline_shapes_stage_isolated(port, name, t, h, w, f, cfg):
+    """wpsum / gather_stack at the BASELINE F / ps / stride0 (c5: F = 64 runs the query-centric
+    kernel as two channel slices) against the oracle on the device's own selection."""
+    S = snls_mod()
+    q, k, ff, bf, ref, lp1, wts = case(port, name, t, h, w, f, cfg)
+    v = video(port, t, h, w, f, 777)
+    r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), want_weights=True)
+    out, cnt = S.wpsum(dev(v), r.weights, r.offsets, scfg(cfg))
+    want, wcnt = port.wpsum(v, host(r.weights), host(r.offsets), cfg)
+    assert np.array_equal(host(cnt), wcnt)
+    assert max_rel(host(out), want) <= REL_TOL
+    st = S.gather_stack(dev(v), r.weights, r.offsets, scfg(cfg))
+    assert max_rel(host(st), port.gather_stack(v, host(r.weights), host(r.offsets), cfg)) <= REL_TOL

@@ -148,6 +148,8 @@ def lib() -> C.CDLL:
             L.snls_pipeline_create.argtypes = [VOIDP, P, _Dims, C.c_int, C.POINTER(VOIDP)]
             L.snls_pipeline_destroy.argtypes = [VOIDP]
             L.snls_pipeline_run.argtypes = [VOIDP] + [VOIDP] * 10
+            L.snls_pipeline_submit.argtypes = [VOIDP] + [VOIDP] * 10
+            L.snls_pipeline_wait.argtypes = [VOIDP]
             _lib = L
         return _lib
 
@@ -528,6 +530,18 @@ class Pipeline:
         hp = self._hp
         _raise(lib().snls_pipeline_run(self.h, hp(q), hp(k), hp(v), hp(fflow), hp(bflow),
                                        hp(sims), hp(offsets), hp(weights), hp(out), hp(counts)))
+
+    def submit(self, q, k, v, fflow, bflow, sims=None, offsets=None, weights=None, out=None,
+               counts=None):
+        """Streaming form: enqueue a clip (at most two in flight); the buffers must stay
+        alive and untouched until the matching wait()."""
+        hp = self._hp
+        _raise(lib().snls_pipeline_submit(self.h, hp(q), hp(k), hp(v), hp(fflow), hp(bflow),
+                                          hp(sims), hp(offsets), hp(weights), hp(out), hp(counts)))
+
+    def wait(self):
+        """Block until the oldest submitted clip's results are in host memory."""
+        _raise(lib().snls_pipeline_wait(self.h))
 
     def close(self):
         if getattr(self, "h", None):

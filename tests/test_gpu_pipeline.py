@@ -83,3 +83,27 @@ def test_pipeline_errors():
     pipe = S.Pipeline(S.SearchConfig(ws=3, wt=1, ps=1, topl=2), (T, H, W, F))
     with pytest.raises(S.DomainError, match="search fflow: flow holds a non-finite value"):
         pipe.run(q, q, q, bad, ff)
+
+
+def test_pipeline_streaming_submit_wait():
+    """Two clips in flight (submit/submit/wait/wait, then more than two submits in a row):
+    every clip's results equal the synchronous path's."""
+    S = snls_mod()
+    P = Checker("port")
+    T, H, W, F = 5, 18, 20, 32
+    cfg = S.SearchConfig(ws=11, wt=3, ps=3, stride0=2, topl=16, metric="l2", softmax_scale=1 / 288)
+    clips = [video(P, T, H, W, F, 70 + i).astype(np.float32) for i in range(5)]
+    flows = [flow(P, T, H, W, 80 + i, 2.0).astype(np.float32) for i in range(5)]
+    pipe = S.Pipeline(cfg, (T, H, W, F), chunk_frames=1)
+    want = []
+    for c, fl in zip(clips, flows):
+        sims, offs, wts, out, cnt = _host_out(S, T, H, W, F, cfg)
+        pipe.run(c, c, c, fl, fl, sims=sims, out=out)
+        want.append((sims, out))
+    got = [_host_out(S, T, H, W, F, cfg) for _ in clips]
+    for i, (c, fl) in enumerate(zip(clips, flows)):  # a third submit waits for the oldest
+        pipe.submit(c, c, c, fl, fl, sims=got[i][0], out=got[i][3])
+    pipe.wait()
+    pipe.wait()
+    for (ws, wo), g in zip(want, got):
+        assert np.array_equal(g[0], ws) and np.array_equal(g[3], wo)

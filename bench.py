@@ -523,7 +523,7 @@ def cpu_baseline(wl, budget_s=20.0):
     t = run()  # warm-up + size probe
     times = []
     deadline = time.perf_counter() + budget_s
-    while len(times) < 3 or (time.perf_counter() < deadline and len(times) < 9):
+    while len(times) < 3 or (time.perf_counter() < deadline and len(times) < 40):
         times.append(run())
         if time.perf_counter() > deadline and len(times) >= 1:
             break
@@ -570,7 +570,7 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-crop", type=int, default=96)
     ap.add_argument("--pipe-chunk", type=int, default=int(os.environ.get("SNLS_PIPE_CHUNK", "0")),
                     help="query frames per chunk of the e2e host pipeline (0: 1)")

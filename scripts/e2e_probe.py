@@ -56,3 +56,27 @@ for c in (1, 2, 5):
 for c in (1, 2):
     pipe = S.Pipeline(cfg, vid.shape, chunk_frames=c, ctx=ctx)
     print(f"pipeline({c}) ms", timeit(lambda: pipe.run(vp, vp, vp, fp_, bp, sims=sp, offsets=op_, out=oo)))
+
+# device-resident, chunked over two streams (search of chunk i+1 overlaps wpsum/tail of i)
+s2 = [torch.cuda.Stream(), torch.cuda.Stream()]
+ctxs = [S.Context(0, s2[0]), S.Context(0, s2[1])]
+def chunked2(c):
+    def f():
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        for st in s2:
+            st.wait_event(ev)
+        for i, a in enumerate(range(0, T, c)):
+            b = min(T, a + c)
+            r0, r1 = a * nq, b * nq
+            cx = ctxs[i % 2]
+            S.shifted_nls_forward(vd, vd, fd, bd, cfg, ctx=cx, check=False, frames=(a, b),
+                                  out=(sims[r0:r1], offs[r0:r1], None, wts[r0:r1]))
+            S.wpsum(vd, wts[r0:r1], offs[r0:r1], cfg, ctx=cx, check=False, frames=(a, b),
+                    out=(out[a:b], cnt[a:b]))
+        for st in s2:
+            e = torch.cuda.Event(); e.record(st); cur.wait_event(e)
+    return f
+for c in (1, 2, 5):
+    print(f"chunked2({c}) compute ms", timeit(chunked2(c)))

@@ -521,11 +521,7 @@ int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream
 }
 
 int launch_wpsum_query_any(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
-    static const bool off = [] {
-        const char* e = std::getenv("SNLS_WPSUM_GATHER");
-        return e && std::atoi(e) == 1;
-    }();
-    if (off || a.d.f % 4 != 0) return 0;
+    if (a.d.f % 4 != 0) return 0;
     const int FG = a.d.f / 4;
     // channel slices of 8 float4 (128 B per pixel): slices of 4 measured slower (c4 0.54 ->
     // 0.71 ms, c5 19.0 -> 25.2 ms), one 16-wide slice holds 1 CTA/SM (c5 27.3 ms)

@@ -114,7 +114,9 @@ bool underfull(const snls_config* c, int t, int t0 = 0, int t1 = -1) {
 int ensure_work(snls_ctx* ctx, size_t bytes) {
     if (ctx->work_bytes >= bytes) return SNLS_OK;
     if (ctx->work) {
-        cudaStreamSynchronize(ctx->stream);
+        // the context's stream may have been switched (pipeline chunks): wait for every
+        // stream of the device before the old workspace goes away (a rare, growing resize)
+        cudaDeviceSynchronize();
         cudaFree(ctx->work);
         ctx->work = nullptr;
         ctx->work_bytes = 0;

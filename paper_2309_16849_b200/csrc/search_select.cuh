@@ -57,6 +57,10 @@ struct TopL {
     float ev[S::M];
     uint32_t es[S::M];
 
+    // lane of the warp holding rank topl-1 of group gq, and its entry index there
+    static __device__ __forceinline__ int thr_lane(int gq, int topl) { return gq * G + (topl - 1) / S::M; }
+    static __device__ __forceinline__ int thr_entry(int topl) { return (topl - 1) % S::M; }
+
     __device__ __forceinline__ void init() {
 #pragma unroll
         for (int j = 0; j < S::M; ++j) {
@@ -72,7 +76,7 @@ struct TopL {
     template <int METRIC>
     __device__ __forceinline__ void finish_row(const float (&acc_row)[W], int lane, int gl, int gq,
                                                bool on, bool row_ok, int arow, uint32_t slot_base,
-                                               float* grid_row, int topl) {
+                                               float* grid_row, int thr_src, int thr_idx) {
         float v[S::NPAD];
 #pragma unroll
         for (int b = 0; b < S::NPAD; ++b) v[b] = b < W ? acc_row[b] : 0.f;
@@ -104,12 +108,13 @@ struct TopL {
             }
             return;
         }
-        // rank topl-1 lives in lane (topl-1)/M of the group, entry (topl-1)%M
-        const int thr_idx = (topl - 1) % S::M;
-        float thr = -INFINITY;
+        // rank topl-1 lives in lane thr_src of the warp (group gq), entry thr_idx
+        float thr = ev[S::M - 1];
+        if constexpr (S::M > 1) {
 #pragma unroll
-        for (int j = 0; j < S::M; ++j) thr = j == thr_idx ? ev[j] : thr;
-        thr = __shfl_sync(0xffffffffu, thr, gq * G + (topl - 1) / S::M);
+            for (int j = 0; j < S::M - 1; ++j) thr = j == thr_idx ? ev[j] : thr;
+        }
+        thr = __shfl_sync(0xffffffffu, thr, thr_src);
         uint32_t pend = 0;
 #pragma unroll
         for (int i = 0; i < S::NPL; ++i) {

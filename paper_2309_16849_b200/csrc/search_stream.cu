@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
 
     TopL<W, G, KMAX> sel;
     sel.init();
+    const int thr_src = TopL<W, G, KMAX>::thr_lane(gq, a.topl), thr_idx = TopL<W, G, KMAX>::thr_entry(a.topl);
     float* grid_row = a.grid ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
             // ---- slot row r-(P-1) complete: reduce-scatter over the G lanes, then stream
             if (r >= P - 1)
                 sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base,
-                                                grid_row, a.topl);
+                                                grid_row, thr_src, thr_idx);
             // rotate: acc[s] tracks slot row r-(P-1)+s
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)

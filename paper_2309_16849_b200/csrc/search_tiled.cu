@@ -48,6 +48,34 @@ __device__ __forceinline__ void lerpv(float (&r)[VEC], const float (&a)[VEC], co
 
 // QREG: the query patch (P x P x VEC per lane) is loaded once into registers instead of
 // being re-read from L1 on every region row (used where it fits: ps = 7 on float2 lanes).
+__device__ __forceinline__ float4 lerp4(const float4& a, const float4& b, const float4& c,
+                                        const float4& d, float w00, float w01, float w10,
+                                        float w11) {
+    float4 r;
+    r.x = fmaf(w11, d.x, fmaf(w10, c.x, fmaf(w01, b.x, w00 * a.x)));
+    r.y = fmaf(w11, d.y, fmaf(w10, c.y, fmaf(w01, b.y, w00 * a.y)));
+    r.z = fmaf(w11, d.z, fmaf(w10, c.z, fmaf(w01, b.z, w00 * a.z)));
+    r.w = fmaf(w11, d.w, fmaf(w10, c.w, fmaf(w01, b.w, w00 * a.w)));
+    return r;
+}
+
+template <int METRIC>
+__device__ __forceinline__ float accum4(float acc, const float4& q, const float4& k) {
+    if (METRIC == SNLS_METRIC_IP) {
+        acc = fmaf(q.x, k.x, acc);
+        acc = fmaf(q.y, k.y, acc);
+        acc = fmaf(q.z, k.z, acc);
+        acc = fmaf(q.w, k.w, acc);
+    } else {  // negated squared L2 accumulated as +sum(d^2); sign applied at emission
+        float d;
+        d = q.x - k.x; acc = fmaf(d, d, acc);
+        d = q.y - k.y; acc = fmaf(d, d, acc);
+        d = q.z - k.z; acc = fmaf(d, d, acc);
+        d = q.w - k.w; acc = fmaf(d, d, acc);
+    }
+    return acc;
+}
+
 template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
@@ -86,6 +114,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
 
     TopL<W, G, KMAX> sel;
     sel.init();
+    const int thr_src = TopL<W, G, KMAX>::thr_lane(gq, a.topl), thr_idx = TopL<W, G, KMAX>::thr_entry(a.topl);
     float* grid_row = a.grid ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
@@ -126,71 +155,112 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
             const unsigned r0 = unsigned(reflect_near(by + r, H)) * rowv;
             const unsigned r1 = unsigned(reflect_near(by + r + 1, H)) * rowv;
-            float kr[R][VEC];
-            float a0[VEC], a1[VEC], b0[VEC], b1[VEC];
-            if (interior) {
-                // no column reflection anywhere in the warp: one base per raw row and
-                // compile-time offsets (LDG [R + imm]) for the ws+ps columns
-                const float* p0 = kframe + size_t(r0 + xb) * VEC;
-                const float* p1 = kframe + size_t(r1 + xb) * VEC;
-                ldv<VEC>(p0, a0);
-                ldv<VEC>(p1, a1);
+            if constexpr (VEC == 4 && !QREG) {
+                // float4-typed registers (this formulation schedules ~2% better on B200 than
+                // the VEC-generic arrays below: fewer dispatch stalls)
+                const float4* kb4 = reinterpret_cast<const float4*>(kframe);
+                float4 kr[R];
+                if (interior) {
+                    const float4* p0 = kb4 + (r0 + xb);
+                    const float4* p1 = kb4 + (r1 + xb);
+                    float4 a0 = __ldg(p0), a1 = __ldg(p1);
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    ldv<VEC>(p0 + (j + 1) * F, b0);
-                    ldv<VEC>(p1 + (j + 1) * F, b1);
-                    lerpv<VEC>(kr[j], a0, b0, a1, b1, w00, w01, w10, w11);
+                    for (int j = 0; j < R; ++j) {
+                        const float4 b0 = __ldg(p0 + (j + 1) * G), b1 = __ldg(p1 + (j + 1) * G);
+                        kr[j] = lerp4(a0, b0, a1, b1, w00, w01, w10, w11);
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                } else {
+                    float4 a0 = __ldg(kb4 + (r0 + xo[0])), a1 = __ldg(kb4 + (r1 + xo[0]));
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) {
-                        a0[v] = b0[v];
-                        a1[v] = b1[v];
+                    for (int j = 0; j < R; ++j) {
+                        const float4 b0 = __ldg(kb4 + (r0 + xo[j + 1]));
+                        const float4 b1 = __ldg(kb4 + (r1 + xo[j + 1]));
+                        kr[j] = lerp4(a0, b0, a1, b1, w00, w01, w10, w11);
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < P; ++s) {
+                    const int arow = r - (P - 1) + s;
+                    if (arow < 0 || arow >= W) continue;  // uniform across the warp
+                    const float* qr = qbase + qrow[P - 1 - s];
+#pragma unroll
+                    for (int px = 0; px < P; ++px) {
+                        const float4 qv = __ldg(reinterpret_cast<const float4*>(qr + qcol[px]));
+#pragma unroll
+                        for (int b = 0; b < W; ++b) acc[s][b] = accum4<METRIC>(acc[s][b], qv, kr[b + px]);
                     }
                 }
             } else {
-                ld(r0 + xo[0], a0);
-                ld(r1 + xo[0], a1);
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    ld(r0 + xo[j + 1], b0);
-                    ld(r1 + xo[j + 1], b1);
-                    lerpv<VEC>(kr[j], a0, b0, a1, b1, w00, w01, w10, w11);
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) {
-                        a0[v] = b0[v];
-                        a1[v] = b1[v];
+                float kr[R][VEC];
+                float a0[VEC], a1[VEC], b0[VEC], b1[VEC];
+                if (interior) {
+                    // no column reflection anywhere in the warp: one base per raw row and
+                    // compile-time offsets (LDG [R + imm]) for the ws+ps columns
+                    const float* p0 = kframe + size_t(r0 + xb) * VEC;
+                    const float* p1 = kframe + size_t(r1 + xb) * VEC;
+                    ldv<VEC>(p0, a0);
+                    ldv<VEC>(p1, a1);
+    #pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        ldv<VEC>(p0 + (j + 1) * F, b0);
+                        ldv<VEC>(p1 + (j + 1) * F, b1);
+                        lerpv<VEC>(kr[j], a0, b0, a1, b1, w00, w01, w10, w11);
+    #pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            a0[v] = b0[v];
+                            a1[v] = b1[v];
+                        }
+                    }
+                } else {
+                    ld(r0 + xo[0], a0);
+                    ld(r1 + xo[0], a1);
+    #pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        ld(r0 + xo[j + 1], b0);
+                        ld(r1 + xo[j + 1], b1);
+                        lerpv<VEC>(kr[j], a0, b0, a1, b1, w00, w01, w10, w11);
+    #pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            a0[v] = b0[v];
+                            a1[v] = b1[v];
+                        }
                     }
                 }
-            }
-            // ---- update the slot rows that read region row r: a = r - (P-1) + s, py = P-1-s
-#pragma unroll
-            for (int s = 0; s < P; ++s) {
-                const int arow = r - (P - 1) + s;
-                if (arow < 0 || arow >= W) continue;  // uniform across the warp
-                const float* qr = qbase + qrow[P - 1 - s];
-#pragma unroll
-                for (int px = 0; px < P; ++px) {
-                    float qv[VEC];
-                    if constexpr (QREG) {
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) qv[v] = qreg[P - 1 - s][px][v];
-                    } else {
-                        ldv<VEC>(qr + qcol[px], qv);
-                    }
-#pragma unroll
-                    for (int b = 0; b < W; ++b)
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) {
-                            if (METRIC == SNLS_METRIC_IP) {
-                                acc[s][b] = fmaf(qv[v], kr[b + px][v], acc[s][b]);
-                            } else {  // negated squared L2 accumulated as +sum(d^2)
-                                const float d = qv[v] - kr[b + px][v];
-                                acc[s][b] = fmaf(d, d, acc[s][b]);
-                            }
+                // ---- update the slot rows that read region row r: a = r - (P-1) + s, py = P-1-s
+    #pragma unroll
+                for (int s = 0; s < P; ++s) {
+                    const int arow = r - (P - 1) + s;
+                    if (arow < 0 || arow >= W) continue;  // uniform across the warp
+                    const float* qr = qbase + qrow[P - 1 - s];
+    #pragma unroll
+                    for (int px = 0; px < P; ++px) {
+                        float qv[VEC];
+                        if constexpr (QREG) {
+    #pragma unroll
+                            for (int v = 0; v < VEC; ++v) qv[v] = qreg[P - 1 - s][px][v];
+                        } else {
+                            ldv<VEC>(qr + qcol[px], qv);
                         }
+    #pragma unroll
+                        for (int b = 0; b < W; ++b)
+    #pragma unroll
+                            for (int v = 0; v < VEC; ++v) {
+                                if (METRIC == SNLS_METRIC_IP) {
+                                    acc[s][b] = fmaf(qv[v], kr[b + px][v], acc[s][b]);
+                                } else {  // negated squared L2 accumulated as +sum(d^2)
+                                    const float d = qv[v] - kr[b + px][v];
+                                    acc[s][b] = fmaf(d, d, acc[s][b]);
+                                }
+                            }
+                    }
                 }
             }
             // ---- slot row r-(P-1) is complete: reduce-scatter over the G lanes, stream
-            if (r >= P - 1) sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base, grid_row, a.topl);
+            if (r >= P - 1) sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base, grid_row, thr_src, thr_idx);
             // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)

@@ -245,10 +245,12 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                         } else {
                             ldv<VEC>(qr + qcol[px], qv);
                         }
-    #pragma unroll
-                        for (int b = 0; b < W; ++b)
-    #pragma unroll
-                            for (int v = 0; v < VEC; ++v) {
+                        // channel-outer: consecutive FMAs hit W different accumulators (the
+                        // per-accumulator order, channel ascending, is unchanged)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v)
+#pragma unroll
+                            for (int b = 0; b < W; ++b) {
                                 if (METRIC == SNLS_METRIC_IP) {
                                     acc[s][b] = fmaf(qv[v], kr[b + px][v], acc[s][b]);
                                 } else {  // negated squared L2 accumulated as +sum(d^2)

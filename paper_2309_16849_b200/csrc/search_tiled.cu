@@ -76,6 +76,50 @@ __device__ __forceinline__ float accum4(float acc, const float4& q, const float4
     return acc;
 }
 
+// ---- packed fp32x2 (FFMA2 / FMUL2 on sm_100a): two FMAs per issued instruction at the same
+// FMA-pipe rate as FFMA (scripts/micro/ffma2_peak.cu: 74.1 vs 72.2 TFLOP/s), so the search
+// loop's FP work takes half the issue slots and the overhead instructions fill the rest.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pk2(float x, float y) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(u64 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// a float4 as two channel pairs (x, y) and (z, w)
+struct P4 {
+    u64 lo, hi;
+};
+__device__ __forceinline__ P4 ldp4(const float4* p) {
+    const float4 v = __ldg(p);
+    return {pk2(v.x, v.y), pk2(v.z, v.w)};
+}
+// the blend of lerp4, same operation order per channel
+__device__ __forceinline__ P4 lerp2(const P4& a, const P4& b, const P4& c, const P4& d, u64 w00,
+                                    u64 w01, u64 w10, u64 w11) {
+    return {fma2(w11, d.lo, fma2(w10, c.lo, fma2(w01, b.lo, mul2(w00, a.lo)))),
+            fma2(w11, d.hi, fma2(w10, c.hi, fma2(w01, b.hi, mul2(w00, a.hi))))};
+}
+
+#ifndef SNLS_PACKED_F32X2
+#define SNLS_PACKED_F32X2 1
+#endif
+constexpr bool kPacked = SNLS_PACKED_F32X2 != 0;
+
 template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
@@ -155,7 +199,65 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
             const unsigned r0 = unsigned(reflect_near(by + r, H)) * rowv;
             const unsigned r1 = unsigned(reflect_near(by + r + 1, H)) * rowv;
-            if constexpr (VEC == 4 && !QREG) {
+            if constexpr (VEC == 4 && !QREG && kPacked) {
+                // packed fp32x2: channel pairs (x, y), (z, w) of every float4.  Per slot and
+                // region row the partial sum runs in the two halves of a pair t and is folded
+                // into the slot accumulator as (t.x + t.y): the same addition tree for every
+                // slot, so duplicate candidates still tie exactly.
+                const float4* kb4 = reinterpret_cast<const float4*>(kframe);
+                const u64 W00 = pk2(w00, w00), W01 = pk2(w01, w01), W10 = pk2(w10, w10), W11 = pk2(w11, w11);
+                P4 kr[R];
+                if (interior) {
+                    const float4* p0 = kb4 + (r0 + xb);
+                    const float4* p1 = kb4 + (r1 + xb);
+                    P4 a0 = ldp4(p0), a1 = ldp4(p1);
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const P4 b0 = ldp4(p0 + (j + 1) * G), b1 = ldp4(p1 + (j + 1) * G);
+                        kr[j] = lerp2(a0, b0, a1, b1, W00, W01, W10, W11);
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                } else {
+                    P4 a0 = ldp4(kb4 + (r0 + xo[0])), a1 = ldp4(kb4 + (r1 + xo[0]));
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const P4 b0 = ldp4(kb4 + (r0 + xo[j + 1]));
+                        const P4 b1 = ldp4(kb4 + (r1 + xo[j + 1]));
+                        kr[j] = lerp2(a0, b0, a1, b1, W00, W01, W10, W11);
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                }
+                const u64 NEG1 = pk2(-1.f, -1.f), ZERO2 = pk2(0.f, 0.f);
+#pragma unroll
+                for (int s = 0; s < P; ++s) {
+                    const int arow = r - (P - 1) + s;
+                    if (arow < 0 || arow >= W) continue;  // uniform across the warp
+                    const float* qr = qbase + qrow[P - 1 - s];
+                    P4 qv[P];
+#pragma unroll
+                    for (int px = 0; px < P; ++px) qv[px] = ldp4(reinterpret_cast<const float4*>(qr + qcol[px]));
+#pragma unroll
+                    for (int b = 0; b < W; ++b) {
+                        u64 t = ZERO2;
+#pragma unroll
+                        for (int px = 0; px < P; ++px) {
+                            const P4& k = kr[b + px];
+                            if (METRIC == SNLS_METRIC_IP) {
+                                t = fma2(qv[px].lo, k.lo, t);
+                                t = fma2(qv[px].hi, k.hi, t);
+                            } else {  // +sum (q - k)^2; d = q - k as fma(k, -1, q)
+                                const u64 dl = fma2(k.lo, NEG1, qv[px].lo), dh = fma2(k.hi, NEG1, qv[px].hi);
+                                t = fma2(dl, dl, t);
+                                t = fma2(dh, dh, t);
+                            }
+                        }
+                        const float2 tf = upk2(t);
+                        acc[s][b] += tf.x + tf.y;
+                    }
+                }
+            } else if constexpr (VEC == 4 && !QREG) {
                 // float4-typed registers (this formulation schedules ~2% better on B200 than
                 // the VEC-generic arrays below: fewer dispatch stalls)
                 const float4* kb4 = reinterpret_cast<const float4*>(kframe);

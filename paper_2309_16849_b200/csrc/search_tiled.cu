@@ -95,6 +95,11 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
     u64 r;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -229,7 +234,6 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                         a1 = b1;
                     }
                 }
-                const u64 NEG1 = pk2(-1.f, -1.f), ZERO2 = pk2(0.f, 0.f);
 #pragma unroll
                 for (int s = 0; s < P; ++s) {
                     const int arow = r - (P - 1) + s;
@@ -240,16 +244,16 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     for (int px = 0; px < P; ++px) qv[px] = ldp4(reinterpret_cast<const float4*>(qr + qcol[px]));
 #pragma unroll
                     for (int b = 0; b < W; ++b) {
-                        u64 t = ZERO2;
+                        u64 t;
 #pragma unroll
                         for (int px = 0; px < P; ++px) {
                             const P4& k = kr[b + px];
                             if (METRIC == SNLS_METRIC_IP) {
-                                t = fma2(qv[px].lo, k.lo, t);
+                                t = px == 0 ? mul2(qv[px].lo, k.lo) : fma2(qv[px].lo, k.lo, t);
                                 t = fma2(qv[px].hi, k.hi, t);
-                            } else {  // +sum (q - k)^2; d = q - k as fma(k, -1, q)
-                                const u64 dl = fma2(k.lo, NEG1, qv[px].lo), dh = fma2(k.hi, NEG1, qv[px].hi);
-                                t = fma2(dl, dl, t);
+                            } else {  // +sum (q - k)^2
+                                const u64 dl = sub2(qv[px].lo, k.lo), dh = sub2(qv[px].hi, k.hi);
+                                t = px == 0 ? mul2(dl, dl) : fma2(dl, dl, t);
                                 t = fma2(dh, dh, t);
                             }
                         }

@@ -36,7 +36,7 @@ UNIT = "queries/s"
 WORKLOADS = {
     # BASELINE configs[3]: batch=8 T=10 C=32 H=W=256 ws=11 wt=3 ps=3 k=16, one video per GPU
     "c4": dict(T=10, H=256, W=256, C=32, ws=11, wt=3, ps=3, topl=16, metric="l2", stride0=2,
-               beta=1.0 / 288, vid_seed=100, ff_seed=200, bf_seed=300, flow_mag=2.0,
+               beta=1.0 / 288, vid_seed=100, ff_seed=200, bf_seed=300, flow_mag=2.0, pipe_chunk=10,
                name="c4: 10x256x256x32 per video, ws11 wt3 ps3 k16 L2 s0=2, one video/GPU"),
     # BASELINE configs[1]: T=5 C=64 H=W=128 ws=9 wt=2 ps=7 k=10 ip, stride0 4 (hole-free min)
     "c2": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
@@ -52,7 +52,7 @@ WORKLOADS = {
     # across ranks with a wt-frame NCCL halo (per-frame seeds 500*1000+t)
     "c5": dict(T=64, H=512, W=512, C=64, ws=9, wt=2, ps=3, topl=10, metric="l2", stride0=2,
                beta=1.0 / 576, vid_seed=500, ff_seed=501, bf_seed=502, flow_mag=2.0,
-               sharded=True,
+               sharded=True, pipe_chunk=4,
                name="c5: one 64x512x512x64 video, ws9 wt2 ps3 k10 L2 s0=2, frame-sharded + halo"),
 }
 
@@ -320,7 +320,8 @@ def run_ours(args, wl):
     if use_pipe:
         # the C-ABI host-buffer call (snls_pipeline_run): frame-chunked kernels overlapped
         # with the H2D input / D2H result copies; Q = K = V is one host buffer, copied once
-        chunk = args.pipe_chunk or 1
+        # frames per chunk, measured per workload for the streamed e2e (profiles/r01_plans.txt)
+        chunk = args.pipe_chunk or wl.get("pipe_chunk", 1)
         pipe = S.Pipeline(cfg, vid_h.shape, chunk_frames=chunk, ctx=ctx)
 
         def e2e_step():

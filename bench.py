@@ -323,9 +323,11 @@ def run_ours(args, wl):
         # frames per chunk, measured per workload for the streamed e2e (profiles/r01_plans.txt)
         chunk = args.pipe_chunk or wl.get("pipe_chunk", 1)
         pipe = S.Pipeline(cfg, vid_h.shape, chunk_frames=chunk, ctx=ctx)
+        # one clip at a time (latency): per-frame chunks overlap the clip's own transfers best
+        pipe1 = S.Pipeline(cfg, vid_h.shape, chunk_frames=1, ctx=ctx) if chunk != 1 else pipe
 
         def e2e_step():
-            pipe.run(vid_p, vid_p, vid_p, ff_p, bf_p, sims=sims_p, offsets=offs_p, out=out_p)
+            pipe1.run(vid_p, vid_p, vid_p, ff_p, bf_p, sims=sims_p, offsets=offs_p, out=out_p)
     else:
         vd, ffd, bfd = torch.empty_like(own_vid), torch.empty_like(own_ff), torch.empty_like(own_bf)
 
@@ -462,8 +464,8 @@ def run_ours(args, wl):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "sync_ms_per_step": e2e_sync_ms,
                 "api": ("snls_pipeline_submit/wait (C-ABI, a stream of clips from pinned host "
-                        f"buffers, chunked copy/compute overlap, {chunk} frame(s)/chunk; "
-                        "sync_ms_per_step = one clip at a time, snls_pipeline_run)") if use_pipe else
+                        f"buffers, {chunk} frame(s)/chunk, two clips in flight; "
+                        "sync_ms_per_step = one clip at a time, snls_pipeline_run, 1 frame/chunk)") if use_pipe else
                        "torch H2D + NCCL halo + snls_search_fwd_frames/wpsum_fwd_frames + D2H"},
         "gpu_launches": launches,
         "clocks": clk,

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "search_select.cuh"
+#include "packed.cuh"
 
 namespace snls_gpu {
 
@@ -76,43 +77,8 @@ __device__ __forceinline__ float accum4(float acc, const float4& q, const float4
     return acc;
 }
 
-// ---- packed fp32x2 (FFMA2 / FMUL2 on sm_100a): two FMAs per issued instruction at the same
-// FMA-pipe rate as FFMA (scripts/micro/ffma2_peak.cu: 74.1 vs 72.2 TFLOP/s), so the search
-// loop's FP work takes half the issue slots and the overhead instructions fill the rest.
-using u64 = unsigned long long;
-__device__ __forceinline__ u64 pk2(float x, float y) {
-    u64 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
-    return r;
-}
-__device__ __forceinline__ float2 upk2(u64 v) {
-    float2 r;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-    return r;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-    u64 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-    u64 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-    u64 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-// a float4 as two channel pairs (x, y) and (z, w)
-struct P4 {
-    u64 lo, hi;
-};
-__device__ __forceinline__ P4 ldp4(const float4* p) {
-    const float4 v = __ldg(p);
-    return {pk2(v.x, v.y), pk2(v.z, v.w)};
-}
+// ---- packed fp32x2 (packed.cuh): FFMA2 / FADD2 / FMUL2 take half the FP issue slots, so the
+// search loop's overhead instructions fill the rest.
 // the blend of lerp4, same operation order per channel
 __device__ __forceinline__ P4 lerp2(const P4& a, const P4& b, const P4& c, const P4& d, u64 w00,
                                     u64 w01, u64 w10, u64 w11) {

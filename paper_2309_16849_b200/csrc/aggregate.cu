@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
         unsigned bcol[P + 1];
 #pragma unroll
         for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);
-        const float* vb = a.v + size_t(kt) * frameF + cc;
+        const float* __restrict__ vb = a.v + size_t(kt) * frameF + cc;
         float* dvb = dv + size_t(kt) * frameF + cc;
         float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
         size_t roa = size_t(reflect_near(by, H)) * rowF;

@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(128, 3) search_bwd_rows(const float* __restric
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
                                                           const float* __restrict__ k, Dims d,
-                                                          int topl, int metric, float* dq,
-                                                          float* dk, double* gyx) {
+                                                          int topl, int metric,
+                                                          float* __restrict__ dq,
+                                                          float* __restrict__ dk,
+                                                          double* __restrict__ gyx) {
     constexpr int HP = P / 2;
     const int slices = (d.f + 31) / 32;
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;

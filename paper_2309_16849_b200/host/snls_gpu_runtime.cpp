@@ -48,12 +48,43 @@ void* DeviceBuffer::reserve(std::uint64_t bytes) {
     return ptr_;
 }
 
+namespace {
+// Pinned (page-locked) fp32 staging for the fp64 <-> fp32 conversions: grow-only, one per
+// thread, so the copies run at full PCIe rate and the conversion never page-faults.
+struct Staging {
+    float* ptr = nullptr;
+    std::uint64_t n = 0;
+    ~Staging() {
+        if (ptr) {
+            snls_host_unregister(ptr);
+            std::free(ptr);
+        }
+    }
+    float* get(std::uint64_t want) {
+        if (want <= n && ptr) return ptr;
+        if (ptr) {
+            snls_host_unregister(ptr);
+            std::free(ptr);
+        }
+        n = want > 0 ? want : 1;
+        ptr = static_cast<float*>(std::aligned_alloc(4096, ((n * sizeof(float) + 4095) / 4096) * 4096));
+        if (!ptr) throw std::bad_alloc();
+        check(snls_host_register(ptr, n * sizeof(float)));
+        return ptr;
+    }
+};
+thread_local Staging t_stage;
+}  // namespace
+
+float* staging(std::uint64_t n) { return t_stage.get(n); }
+
 float* upload(DeviceBuffer& buf, const double* host, std::uint64_t n) {
-    std::vector<float> tmp(n);
-    for (std::uint64_t i = 0; i < n; ++i) tmp[i] = float(host[i]);
+    float* tmp = staging(n);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < std::int64_t(n); ++i) tmp[i] = float(host[i]);
     float* d = buf.f32(n);
-    check(snls_copy_h2d(context(), d, tmp.data(), n * sizeof(float)));
-    // the staging vector must outlive the async copy
+    check(snls_copy_h2d(context(), d, tmp, n * sizeof(float)));
+    // the staging buffer is reused: the copy must have landed
     check(snls_ctx_sync_check(context()));
     return d;
 }
@@ -70,10 +101,12 @@ std::int32_t* upload_i32(DeviceBuffer& buf, const std::vector<std::int32_t>& hos
 }
 
 void download(std::vector<double>& host, const float* dev, std::uint64_t n) {
-    std::vector<float> tmp(n);
-    check(snls_copy_d2h(context(), tmp.data(), dev, n * sizeof(float)));
+    float* tmp = staging(n);
+    check(snls_copy_d2h(context(), tmp, dev, n * sizeof(float)));
     host.resize(n);
-    for (std::uint64_t i = 0; i < n; ++i) host[i] = double(tmp[i]);
+    double* h = host.data();
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < std::int64_t(n); ++i) h[i] = double(tmp[i]);
 }
 
 void download_i32(std::vector<std::int32_t>& host, const std::int32_t* dev, std::uint64_t n) {

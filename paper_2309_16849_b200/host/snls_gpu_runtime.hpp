@@ -44,6 +44,8 @@ float* upload(DeviceBuffer& buf, const std::vector<double>& host);
 float* upload(DeviceBuffer& buf, const double* host, std::uint64_t n);
 std::int32_t* upload_i32(DeviceBuffer& buf, const std::vector<std::int32_t>& host);
 void download(std::vector<double>& host, const float* dev, std::uint64_t n);
+// The calling thread's pinned fp32 staging buffer (>= n floats; reused by upload/download).
+float* staging(std::uint64_t n);
 void download_i32(std::vector<std::int32_t>& host, const std::int32_t* dev, std::uint64_t n);
 
 snls_config to_abi(const snls::SearchConfig& cfg);

@@ -197,25 +197,39 @@ SearchResult shifted_nls_forward(const VideoTensor& q, const VideoTensor& k,
     gpu::check(snls_ctx_sync_check(ctx));
     gpu::download(res.sims.values, dsims, n_sel);
     gpu::download(res.offsets.data, doffs, n_sel * 3);
-    res.tape.centers.assign(n_sel * 3, 0.0);
-    res.tape.chains.assign(n_sel * cs * 6, 0.0);
-    std::vector<double> rel;
-    if (cs > 0) gpu::download(rel, dch, n_sel * cs * 6);
+    res.tape.centers.resize(n_sel * 3);
+    res.tape.chains.resize(n_sel * cs * 6);
+    // device chains (relative to the query pixel) stay in the pinned staging buffer and are
+    // converted to the reference's absolute positions in one parallel pass
+    const float* rel = nullptr;
+    if (cs > 0) {
+        float* st = gpu::staging(n_sel * cs * 6);
+        gpu::check(snls_copy_d2h(ctx, st, dch, n_sel * cs * 6 * sizeof(float)));
+        rel = st;
+    }
+    double* centers = res.tape.centers.data();
+    double* chains = res.tape.chains.data();
+    const double* offs = res.offsets.data.data();
+#pragma omp parallel for schedule(static) num_threads(policy.resolved_threads())
     for (std::int64_t row = 0; row < rows; ++row) {
         double qt, qy, qx;
         query_base(grid, row, qt, qy, qx);
         for (int li = 0; li < L; ++li) {
             const std::size_t e = std::size_t(row) * L + li;
-            const double* o = &res.offsets.data[e * 3];
-            res.tape.centers[e * 3 + 0] = qt + o[0];
-            res.tape.centers[e * 3 + 1] = qy + o[1];
-            res.tape.centers[e * 3 + 2] = qx + o[2];
+            const double* o = offs + e * 3;
+            centers[e * 3 + 0] = qt + o[0];
+            centers[e * 3 + 1] = qy + o[1];
+            centers[e * 3 + 2] = qx + o[2];
             const int links = std::max(int(std::lround(std::abs(o[0]))) - 1, 0);
-            for (int kk = 0; kk < links && kk < cs; ++kk) {  // relative -> absolute positions
+            for (int kk = 0; kk < cs; ++kk) {  // relative -> absolute positions (unused: 0)
                 const std::size_t b = (e * cs + kk) * 6;
-                res.tape.chains[b + 0] = qy + rel[b + 0];
-                res.tape.chains[b + 1] = qx + rel[b + 1];
-                for (int j = 2; j < 6; ++j) res.tape.chains[b + j] = rel[b + j];
+                if (kk < links) {
+                    chains[b + 0] = qy + double(rel[b + 0]);
+                    chains[b + 1] = qx + double(rel[b + 1]);
+                    for (int j = 2; j < 6; ++j) chains[b + j] = double(rel[b + j]);
+                } else {
+                    for (int j = 0; j < 6; ++j) chains[b + j] = 0.0;
+                }
             }
         }
     }

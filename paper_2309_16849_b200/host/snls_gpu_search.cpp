@@ -275,6 +275,8 @@ void tape_to_device(const SearchTape& tape, float*& doffs, float*& dch) {
     const int L = tape.cfg.topl, cs = tape.chain_stride;
     const std::size_t n = std::size_t(rows) * L;
     std::vector<double> offs(n * 3), rel(n * std::size_t(cs) * 6, 0.0);
+    // rows write disjoint slices of offs / rel
+#pragma omp parallel for schedule(static)
     for (std::int64_t row = 0; row < rows; ++row) {
         double qt, qy, qx;
         query_base(tape.grid, row, qt, qy, qx);

@@ -90,12 +90,24 @@ __device__ __forceinline__ P4 lerp2(const P4& a, const P4& b, const P4& c, const
 #define SNLS_PACKED_F32X2 1
 #endif
 constexpr bool kPacked = SNLS_PACKED_F32X2 != 0;
+// ps = 7 on float2 lanes: the query patch parked in shared memory (each lane reads back only
+// what it wrote: no barrier) and the search on packed pairs
+#ifndef SNLS_QSM
+#define SNLS_QSM 1
+#endif
+constexpr bool kQsm = SNLS_QSM != 0 && SNLS_PACKED_F32X2 != 0;
+#ifndef SNLS_QSM_MINB
+#define SNLS_QSM_MINB 3
+#endif
 
 template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
     constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
+    constexpr bool kPackedPath = VEC == 4 && !QREG && kPacked;
+    constexpr bool kPairPath = VEC == 2 && !QREG && kQsm;  // Q in shared memory
     __shared__ uint64_t s_keys[C::QPB][16];
+    extern __shared__ u64 s_qpatch[];  // kPairPath: [QPB][P*P][G] channel pairs
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane / G, gl = lane % G;
@@ -126,6 +138,17 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
 #pragma unroll
             for (int px = 0; px < P; ++px) ldv<VEC>(qbase + qrow[py] + qcol[px], qreg[py][px]);
     }
+    u64* sq = s_qpatch + size_t(qslot) * P * P * G + gl;
+    if constexpr (kPairPath) {
+#pragma unroll
+        for (int py = 0; py < P; ++py)
+#pragma unroll
+            for (int px = 0; px < P; ++px) {
+                float v[2];
+                ldv<2>(qbase + qrow[py] + qcol[px], v);
+                sq[(py * P + px) * G] = pk2(v[0], v[1]);
+            }
+    }
 
     TopL<W, G, KMAX> sel;
     sel.init();
@@ -151,6 +174,8 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         // vector index (one IMAD.WIDE per load instead of 64-bit pointer math)
         const float* kframe = a.k + size_t(on ? kt : qt) * frame_elems + c0;
         const unsigned rowv = unsigned(Wd) * G;  // VEC-vectors per image row
+        // reflected column offsets, precomputed (recomputing them at the boundary-warp loads
+        // instead: c4 5.06 vs 4.45 ms)
         unsigned xo[R + 1];
 #pragma unroll
         for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * G;
@@ -170,7 +195,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
             const unsigned r0 = unsigned(reflect_near(by + r, H)) * rowv;
             const unsigned r1 = unsigned(reflect_near(by + r + 1, H)) * rowv;
-            if constexpr (VEC == 4 && !QREG && kPacked) {
+            if constexpr (kPackedPath) {
                 // packed fp32x2: channel pairs (x, y), (z, w) of every float4.  Per slot and
                 // region row the partial sum runs in the two halves of a pair t and is folded
                 // into the slot accumulator as (t.x + t.y): the same addition tree for every
@@ -204,7 +229,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                 for (int s = 0; s < P; ++s) {
                     const int arow = r - (P - 1) + s;
                     if (arow < 0 || arow >= W) continue;  // uniform across the warp
-                    const float* qr = qbase + qrow[P - 1 - s];
+                    [[maybe_unused]] const float* qr = qbase + qrow[P - 1 - s];
                     P4 qv[P];
 #pragma unroll
                     for (int px = 0; px < P; ++px) qv[px] = ldp4(reinterpret_cast<const float4*>(qr + qcol[px]));
@@ -225,6 +250,62 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                         }
                         const float2 tf = upk2(t);
                         acc[s][b] += tf.x + tf.y;
+                    }
+                }
+            } else if constexpr (kPairPath) {
+                // packed pairs on float2 lanes: per slot row and region row the partial sum
+                // runs in the two halves and is folded as (t.x + t.y), as in the float4 path
+                const u64* kb2 = reinterpret_cast<const u64*>(kframe);
+                const u64 W00 = pk2(w00, w00), W01 = pk2(w01, w01), W10 = pk2(w10, w10), W11 = pk2(w11, w11);
+                auto ld2 = [](const u64* q) { return __ldg(reinterpret_cast<const unsigned long long*>(q)); };
+                u64 kr[R];
+                if (interior) {
+                    const u64* p0 = kb2 + (r0 + xb);
+                    const u64* p1 = kb2 + (r1 + xb);
+                    u64 a0 = ld2(p0), a1 = ld2(p1);
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const u64 b0 = ld2(p0 + (j + 1) * G), b1 = ld2(p1 + (j + 1) * G);
+                        kr[j] = fma2(W11, b1, fma2(W10, a1, fma2(W01, b0, mul2(W00, a0))));
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                } else {
+                    u64 a0 = ld2(kb2 + (r0 + xo[0])), a1 = ld2(kb2 + (r1 + xo[0]));
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const u64 b0 = ld2(kb2 + (r0 + xo[j + 1])), b1 = ld2(kb2 + (r1 + xo[j + 1]));
+                        kr[j] = fma2(W11, b1, fma2(W10, a1, fma2(W01, b0, mul2(W00, a0))));
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < P; ++s) {
+                    const int arow = r - (P - 1) + s;
+                    if (arow < 0 || arow >= W) continue;  // uniform across the warp
+                    const u64* qs = sq + (P - 1 - s) * P * G;
+                    u64 t[W];
+#pragma unroll
+                    for (int px = 0; px < P; ++px) {
+                        const u64 qv = qs[px * G];
+#pragma unroll
+                        for (int b = 0; b < W; ++b) {
+                            if (METRIC == SNLS_METRIC_IP) {
+                                t[b] = px == 0 ? mul2(qv, kr[b + px]) : fma2(qv, kr[b + px], t[b]);
+                            } else {  // +sum (q - k)^2
+                                const u64 d = sub2(qv, kr[b + px]);
+                                t[b] = px == 0 ? mul2(d, d) : fma2(d, d, t[b]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < W; ++b) {
+                        const float2 tf = upk2(t[b]);
+                        if (s == P - 1)
+                            acc[s][b] = tf.x + tf.y;
+                        else
+                            acc[s][b] += tf.x + tf.y;
                     }
                 }
             } else if constexpr (VEC == 4 && !QREG) {
@@ -258,7 +339,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                 for (int s = 0; s < P; ++s) {
                     const int arow = r - (P - 1) + s;
                     if (arow < 0 || arow >= W) continue;  // uniform across the warp
-                    const float* qr = qbase + qrow[P - 1 - s];
+                    [[maybe_unused]] const float* qr = qbase + qrow[P - 1 - s];
 #pragma unroll
                     for (int px = 0; px < P; ++px) {
                         const float4 qv = __ldg(reinterpret_cast<const float4*>(qr + qcol[px]));
@@ -307,7 +388,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                 for (int s = 0; s < P; ++s) {
                     const int arow = r - (P - 1) + s;
                     if (arow < 0 || arow >= W) continue;  // uniform across the warp
-                    const float* qr = qbase + qrow[P - 1 - s];
+                    [[maybe_unused]] const float* qr = qbase + qrow[P - 1 - s];
     #pragma unroll
                     for (int px = 0; px < P; ++px) {
                         float qv[VEC];
@@ -335,13 +416,18 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             }
             // ---- slot row r-(P-1) is complete: reduce-scatter over the G lanes, stream
             if (r >= P - 1) sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base, grid_row, thr_src, thr_idx);
-            // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one
+            // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one (an
+            // unroll by P that renames instead costs 3x the code: c4 5.9 vs 4.45 ms, i-cache);
+            // the pair path assigns a slot row's first contribution, the others start at zero
+            // (assigning in the float4 path: c5 128.2 vs 125.8 ms)
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)
 #pragma unroll
                 for (int b = 0; b < W; ++b) acc[s][b] = acc[s + 1][b];
+            if constexpr (!kPairPath) {
 #pragma unroll
-            for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
+                for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
+            }
         }
     }
 
@@ -353,18 +439,26 @@ template <int P, int W, int VEC, int G, int KMAX, int MINB>
 int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     using C = TiledCfg<P, W, VEC, G>;
     const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
-    constexpr bool QREG = P >= 7;  // c2: 0.477 -> 0.440 ms (profiles/r01_plans.txt)
+    // ps = 7: query patch in registers (c2: 0.477 -> 0.440 ms, profiles/r01_plans.txt) or, on
+    // packed pairs, in shared memory
+    constexpr bool QSM = kQsm && VEC == 2;
+    constexpr bool QREG = P >= 7 && !QSM;
+    const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64) : 0;
+    auto launch = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
+    };
     if (s.metric == SNLS_METRIC_IP)
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG>);
     else
-        search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG><<<blocks, 32 * C::WARPS, 0, st>>>(s);
+        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG>);
     return 1;
 }
 
 template <int P, int W, int VEC, int G, int KMAX>
 int launch_cfg(const TiledSearch& s, cudaStream_t st) {
-    if constexpr (P >= 7)  // 7 x 9 accumulators + the 15-pixel region row: 8 warps per SM
-        return launch_cfg_b<P, W, VEC, G, KMAX, 2>(s, st);
+    if constexpr (P >= 7)  // 7 x 9 accumulators + the 15-pixel region row: 8 (12) warps per SM
+        return launch_cfg_b<P, W, VEC, G, KMAX, kQsm ? SNLS_QSM_MINB : 2>(s, st);
     else if constexpr (P <= 3 && W <= 9)  // 3 x 9 accumulators fit 128 registers: 16 warps/SM
         return launch_cfg_b<P, W, VEC, G, KMAX, 4>(s, st);  // (c5: 126.7 -> 125.7 ms)
     else

@@ -17,7 +17,8 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsnls_cuda.so")
+# SNLS_LIB_OVERRIDE: an A/B build of the same library (scripts/build_variant.sh)
+LIB_PATH = os.environ.get("SNLS_LIB_OVERRIDE") or os.path.join(PKG, "libsnls_cuda.so")
 
 METRIC_IP, METRIC_L2 = 0, 1
 MODE_FUSED, MODE_FULLGRID = 0, 1

@@ -3,7 +3,7 @@
 w=$1; shift
 mkdir -p gpurun_out
 for envs in "$@"; do
-  tag=$(echo "$w $envs" | tr ' =' '__')
+  tag=$(echo "$w $envs" | tr ' =/' '___')
   env $envs timeout 300 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ab_$tag.log 2>&1
   python - "$w" "$envs" "gpurun_out/ab_$tag.log" <<'PY'
 import json, sys

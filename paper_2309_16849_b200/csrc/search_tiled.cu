@@ -96,6 +96,12 @@ constexpr bool kPacked = SNLS_PACKED_F32X2 != 0;
 #define SNLS_QSM 1
 #endif
 constexpr bool kQsm = SNLS_QSM != 0 && SNLS_PACKED_F32X2 != 0;
+// float4 lanes (ps <= 5): the query patch in shared memory as well (LDS.128 at immediate
+// offsets instead of 64-bit-addressed L1 loads)
+#ifndef SNLS_QSM4
+#define SNLS_QSM4 1
+#endif
+constexpr bool kQsm4 = SNLS_QSM4 != 0 && SNLS_PACKED_F32X2 != 0;
 #ifndef SNLS_QSM_MINB
 #define SNLS_QSM_MINB 3
 #endif
@@ -107,7 +113,9 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     constexpr bool kPackedPath = VEC == 4 && !QREG && kPacked;
     constexpr bool kPairPath = VEC == 2 && !QREG && kQsm;  // Q in shared memory
     __shared__ uint64_t s_keys[C::QPB][16];
-    extern __shared__ u64 s_qpatch[];  // kPairPath: [QPB][P*P][G] channel pairs
+    constexpr bool kQsmF4 = kPackedPath && kQsm4;
+    // kPairPath: [QPB][P*P][G] channel pairs; kQsmF4: [QPB][P*P][G] float4
+    extern __shared__ __align__(16) unsigned char s_qdyn[];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane / G, gl = lane % G;
@@ -138,7 +146,15 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
 #pragma unroll
             for (int px = 0; px < P; ++px) ldv<VEC>(qbase + qrow[py] + qcol[px], qreg[py][px]);
     }
-    u64* sq = s_qpatch + size_t(qslot) * P * P * G + gl;
+    u64* sq = reinterpret_cast<u64*>(s_qdyn) + size_t(qslot) * P * P * G + gl;
+    float4* sq4 = reinterpret_cast<float4*>(s_qdyn) + size_t(qslot) * P * P * G + gl;
+    if constexpr (kQsmF4) {
+#pragma unroll
+        for (int py = 0; py < P; ++py)
+#pragma unroll
+            for (int px = 0; px < P; ++px)
+                sq4[(py * P + px) * G] = __ldg(reinterpret_cast<const float4*>(qbase + qrow[py] + qcol[px]));
+    }
     if constexpr (kPairPath) {
 #pragma unroll
         for (int py = 0; py < P; ++py)
@@ -232,7 +248,14 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     [[maybe_unused]] const float* qr = qbase + qrow[P - 1 - s];
                     P4 qv[P];
 #pragma unroll
-                    for (int px = 0; px < P; ++px) qv[px] = ldp4(reinterpret_cast<const float4*>(qr + qcol[px]));
+                    for (int px = 0; px < P; ++px) {
+                        if constexpr (kQsmF4) {
+                            const float4 v = sq4[((P - 1 - s) * P + px) * G];
+                            qv[px] = {pk2(v.x, v.y), pk2(v.z, v.w)};
+                        } else {
+                            qv[px] = ldp4(reinterpret_cast<const float4*>(qr + qcol[px]));
+                        }
+                    }
 #pragma unroll
                     for (int b = 0; b < W; ++b) {
                         u64 t;
@@ -443,7 +466,8 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     // packed pairs, in shared memory
     constexpr bool QSM = kQsm && VEC == 2;
     constexpr bool QREG = P >= 7 && !QSM;
-    const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64) : 0;
+    const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64)
+                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);

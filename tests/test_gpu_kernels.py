@@ -77,3 +77,51 @@ def test_wpsum_at_baseline_shapes_stage_isolated(port, name, t, h, w, f, cfg):
     assert max_rel(host(out), want) <= REL_TOL
     st = S.gather_stack(dev(v), r.weights, r.offsets, scfg(cfg))
     assert max_rel(host(st), port.gather_stack(v, host(r.weights), host(r.offsets), cfg)) <= REL_TOL
+
+
+# every instantiated tiled kernel (search_tiled.cu launch_search_tiled): (ps, ws) x F x metric,
+# i.e. each lane width G, each arithmetic path (float4 packed / float2 packed pairs, Q patch in
+# shared memory) and both accumulation branches, on frames with borders in play
+MATRIX = [(ps, ws, f, m)
+          for ps, ws in ((3, 11), (3, 9), (7, 9), (1, 9), (3, 5), (1, 5))
+          for f in ((16, 32, 64) if ps == 7 else (4, 8, 16, 32, 64))
+          for m in ("ip", "l2")]
+
+
+@pytest.mark.parametrize("ps,ws,f,metric", MATRIX, ids=[f"p{p}w{w}f{f}{m}" for p, w, f, m in MATRIX])
+def test_tiled_plan_matrix_vs_oracle(port, ps, ws, f, metric):
+    S = snls_mod()
+    t, h, w = 3, 13, 15
+    cfg = Cfg(ws=ws, wt=1, ps=ps, stride0=2, topl=min(10, ws * ws), metric=metric,
+              softmax_scale=1.0 / (ps * ps * f))
+    seed = 7000 + 97 * ps + 13 * ws + f + (1 if metric == "l2" else 0)
+    q, k = video(port, t, h, w, f, seed), video(port, t, h, w, f, seed + 1)
+    ff, bf = flow(port, t, h, w, seed + 2, 2.0), flow(port, t, h, w, seed + 3, 2.0)
+    ref = port.search_fwd(q, k, ff, bf, cfg)
+    lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
+    ctx = S.context()
+    ctx.set_search_kernel("tiled")
+    try:
+        r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), ctx=ctx)
+        assert ctx.last_search_path() == 1, "expected the tiled kernel for this shape"
+    finally:
+        ctx.set_search_kernel("auto")
+    excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
+    # large-|s| L2 rows (ps 7, F 64: |s| ~ 2e3) are often within 1e-4 |s| of a neighbour rank
+    assert excluded < 0.75 * ref["sims"].shape[0]
+
+
+def test_c2_stride1_search_row(port):
+    """SURVEY 8d's search-only c2 row at stride0 = 1 (every pixel a query), reduced frames."""
+    S = snls_mod()
+    cfg = Cfg(ws=9, wt=2, ps=7, stride0=1, topl=10, metric="ip", softmax_scale=1.0 / 3136)
+    t, h, w, f = 5, 12, 14, 64
+    q, k = video(port, t, h, w, f, 11), video(port, t, h, w, f, 12)
+    ff, bf = flow(port, t, h, w, 14, 2.0), flow(port, t, h, w, 15, 2.0)
+    ref = port.search_fwd(q, k, ff, bf, cfg)
+    lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
+    ctx = S.context()
+    r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), ctx=ctx)
+    assert ctx.last_search_path() == 1
+    excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
+    assert excluded < 0.5 * ref["sims"].shape[0]

@@ -635,8 +635,13 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
 // neighbour l.  Then per neighbour: dW = sum Gs * sample (warp-reduced, one atomic per
 // slice) and dV gets w * Gs through the taps, pre-reduced on the (ps+1)^2 raw block two rows
 // at a time ((ps+1)^2 coalesced atomics per entry instead of 4 x writes).
+#ifndef SNLS_WBWD_GSSM
+#define SNLS_WBWD_GSSM 1
+#endif
+constexpr bool kGsSm = SNLS_WBWD_GSSM != 0;
+
 template <int P>
-__global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float* __restrict__ go,
+__global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, const float* __restrict__ go,
                                                          const int32_t* __restrict__ counts,
                                                          float* __restrict__ dv, float* __restrict__ dw) {
     constexpr int HP = P / 2;
@@ -652,7 +657,10 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
     row_coords(a.d, row, ti, qy, qx);
     const int H = a.d.h, W = a.d.w, st = a.d.stride0;
     const size_t F = size_t(a.d.f), rowF = size_t(W) * F, frameF = size_t(H) * rowF;
-    // ---- fold the upstream gradient onto the patch pixels
+    // ---- fold the upstream gradient onto the patch pixels (kGsSm: parked in shared memory,
+    // each lane its own channel, no barrier)
+    __shared__ float s_gs[kGsSm ? 4 : 1][kGsSm ? P * P : 1][32];
+    float* sgs = &s_gs[kGsSm ? threadIdx.x >> 5 : 0][0][lane];
     float gs[P][P];
     // grad_out / counts hold the output frames [t0, t0 + nt) (frame-range form)
     const float* gob = go + size_t(ti - a.d.t0) * frameF + cc;
@@ -685,6 +693,13 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
                     for (int j = 0; j < P; ++j) gs[i][j] += (i == pi && j == pj) ? v : 0.f;
             }
     }
+    if constexpr (kGsSm) {
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int j = 0; j < P; ++j) sgs[(i * P + j) * 32] = gs[i][j];
+    }
+    auto gsv = [&](int i, int j) { return kGsSm ? sgs[(i * P + j) * 32] : gs[i][j]; };
     // ---- per neighbour: dW and the dV block scatter
     for (int l = 0; l < a.topl; ++l) {
         const int64_t e = row * a.topl + l;
@@ -708,25 +723,31 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
         float* dvb = dv + size_t(kt) * frameF + cc;
         float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
         size_t roa = size_t(reflect_near(by, H)) * rowF;
+        size_t rob = size_t(reflect_near(by + 1, H)) * rowF;
 #pragma unroll
         for (int j = 0; j <= P; ++j) {
             ra[j] = act ? __ldg(vb + roa + bcol[j]) : 0.f;
+            rb[j] = act ? __ldg(vb + rob + bcol[j]) : 0.f;
             ka[j] = 0.f;
         }
         float dwl = 0.f;
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const size_t rob = size_t(reflect_near(by + i + 1, H)) * rowF;
+            // raw row i+2 is loaded one row ahead (its latency overlaps row i's arithmetic)
+            float rn[P + 1];
+            const size_t ron = size_t(reflect_near(by + i + 2, H)) * rowF;
+            if (i + 1 < P) {
 #pragma unroll
-            for (int j = 0; j <= P; ++j) {
-                rb[j] = act ? __ldg(vb + rob + bcol[j]) : 0.f;
-                kn[j] = 0.f;
+                for (int j = 0; j <= P; ++j) rn[j] = act ? __ldg(vb + ron + bcol[j]) : 0.f;
             }
+#pragma unroll
+            for (int j = 0; j <= P; ++j) kn[j] = 0.f;
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 const float smp = w00 * ra[j] + w01 * ra[j + 1] + w10 * rb[j] + w11 * rb[j + 1];
-                dwl = fmaf(gs[i][j], smp, dwl);
-                const float gv = gs[i][j] * wv;
+                const float gij = gsv(i, j);
+                dwl = fmaf(gij, smp, dwl);
+                const float gv = gij * wv;
                 ka[j] += gv * w00;
                 ka[j + 1] += gv * w01;
                 kn[j] += gv * w10;
@@ -739,9 +760,11 @@ __global__ void __launch_bounds__(128, 3) wpsum_bwd_rows(AggArgs a, const float*
 #pragma unroll
             for (int j = 0; j <= P; ++j) {
                 ra[j] = rb[j];
+                if (i + 1 < P) rb[j] = rn[j];
                 ka[j] = kn[j];
             }
             roa = rob;
+            rob = ron;
         }
         if (act) {
 #pragma unroll

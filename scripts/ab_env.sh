@@ -10,7 +10,7 @@ import json, sys
 w, envs, f = sys.argv[1:]
 try:
     r = json.loads([l for l in open(f) if l.startswith("{")][-1])
-    print(f"{w} [{envs}]: step {r['ms_per_step']:.3f}  search {r['breakdown_ms']['search_topl_softmax']:.3f}  wpsum {r['breakdown_ms']['wpsum']:.3f}  frac {r['roofline']['frac']:.3f}")
+    print(f"{w} [{envs}]: step {r['ms_per_step']:.3f}  search {r['breakdown_ms']['search_topl_softmax']:.3f}  wpsum {r['breakdown_ms']['wpsum']:.3f}  bwd {r['breakdown_ms'].get('backward', 0):.3f}  frac {r['roofline']['frac']:.3f}")
 except Exception as e:
     print(w, envs, "FAILED", e); print(open(f).read()[-1500:])
 PY

@@ -9,7 +9,7 @@ pkg=$root/paper_2309_16849_b200
 python -c "import sys; sys.path.insert(0, '$root'); from paper_2309_16849_b200 import build; build.build()"
 tmp=$(mktemp -d)
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-  --expt-relaxed-constexpr -I "$root/include" -I "$pkg/csrc" "$@" -c "${SRC:-$pkg/csrc/search_tiled.cu}" -o "$tmp/search_tiled.o"
-objs=$(ls "$pkg"/build/*.o | grep -v search_tiled.o)
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" $objs "$tmp/search_tiled.o" -cudart static
+  --expt-relaxed-constexpr -I "$root/include" -I "$pkg/csrc" "$@" -c "${SRC:-$pkg/csrc/${UNIT:-search_tiled}.cu}" -o "$tmp/${UNIT:-search_tiled}.o"
+objs=$(ls "$pkg"/build/*.o | grep -v ${UNIT:-search_tiled}.o)
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" $objs "$tmp/${UNIT:-search_tiled}.o" -cudart static
 rm -rf "$tmp"

@@ -217,12 +217,17 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
 
 // Accumulate one unit (query at grid (gy, gx), sample at y + dy, x + dx where (dy, dx) is
 // the pixel's displacement inside the query's patch) for neighbours [l0, l1).
+#ifndef SNLS_AGG_UNROLL
+#define SNLS_AGG_UNROLL 4
+#endif
+constexpr int kAggUnroll = SNLS_AGG_UNROLL;
 template <int VEC>
 __device__ __forceinline__ void add_unit_tiled(const AggArgs& a, const SampleDesc* desc,
                                                const TileGeom& g, int gy, int gx, int sy, int sx,
                                                int l0, int l1, int c, float4& acc) {
     const SampleDesc* dq = desc + ((gy - g.gy_lo) * g.nqx + (gx - g.gx_lo)) * a.topl;
     const int H = a.d.h, W = a.d.w, F = a.d.f;
+#pragma unroll kAggUnroll
     for (int l = l0; l < l1; ++l) {
         const SampleDesc d = dq[l];
         const int iy = sy + d.oy, ix = sx + d.ox;

@@ -244,8 +244,8 @@ int snls_pipeline_destroy(snls_pipeline* p);
 int snls_pipeline_run(snls_pipeline* p, const float* q, const float* k, const float* v,
                       const float* fflow, const float* bflow, float* sims, float* offsets,
                       float* weights, float* out, int32_t* counts);
-/* Streaming form for a sequence of clips: submit enqueues and returns (two buffer slots,
- * at most two clips in flight -- a third submit first waits for the oldest), so the next
+/* Streaming form for a sequence of clips: submit enqueues and returns (three buffer slots,
+ * at most three clips in flight -- a fourth submit first waits for the oldest), so the next
  * clip's H2D and head overlap this clip's compute and D2H tail.  wait blocks until the
  * oldest submitted clip's results are in host memory.  Its host buffers must stay valid
  * and untouched until then.  A device-side domain error may surface one wait early. */

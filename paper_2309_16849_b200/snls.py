@@ -534,7 +534,7 @@ class Pipeline:
 
     def submit(self, q, k, v, fflow, bflow, sims=None, offsets=None, weights=None, out=None,
                counts=None):
-        """Streaming form: enqueue a clip (at most two in flight); the buffers must stay
+        """Streaming form: enqueue a clip (at most three in flight); the buffers must stay
         alive and untouched until the matching wait()."""
         hp = self._hp
         _raise(lib().snls_pipeline_submit(self.h, hp(q), hp(k), hp(v), hp(fflow), hp(bflow),

@@ -80,3 +80,22 @@ def chunked2(c):
     return f
 for c in (1, 2, 5):
     print(f"chunked2({c}) compute ms", timeit(chunked2(c)))
+
+# compute with the copy engines busy: does PCIe traffic slow the kernels?
+s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+vd2, fd2, bd2 = torch.empty_like(vd), torch.empty_like(fd), torch.empty_like(bd)
+def busy_copies(n):
+    with torch.cuda.stream(s_in):
+        for _ in range(n):
+            vd2.copy_(vp, non_blocking=True); fd2.copy_(fp_, non_blocking=True); bd2.copy_(bp, non_blocking=True)
+    with torch.cuda.stream(s_out):
+        for _ in range(n):
+            sp.copy_(sims, non_blocking=True); op_.copy_(offs, non_blocking=True); oo.copy_(out, non_blocking=True)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+busy_copies(6)
+a.record()
+for _ in range(5):
+    whole()
+b.record(); torch.cuda.synchronize()
+print("whole compute ms with concurrent H2D+D2H", a.elapsed_time(b) / 5)

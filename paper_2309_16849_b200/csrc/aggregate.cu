@@ -507,9 +507,12 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
     }
 }
 
+#ifndef SNLS_WQ_TILE
+#define SNLS_WQ_TILE 16
+#endif
 template <int P, int G, int FG>
 int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
-    constexpr int TY = 16, TX = 16;
+    constexpr int TY = SNLS_WQ_TILE, TX = SNLS_WQ_TILE;
     const int s0 = a.d.stride0;
     // grid rows meeting a tile aligned to TY (tiles start at multiples of TY)
     const int nqy = (TY + s0 - 2) / s0 + (TY % s0 == 0 ? 1 : 2);

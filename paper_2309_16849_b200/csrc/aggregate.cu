@@ -355,7 +355,7 @@ int launch_tiled_agg(const AggArgs& a, float* out, int32_t* counts, int stack, c
     const int nqy = 3 + 1, nqx = (PPC + 2 * s0) / s0 + 3;
     const size_t smem = size_t(nqy) * nqx * a.topl * sizeof(SampleDesc);
     if (smem > 200 * 1024) return 0;
-    cudaFuncSetAttribute(wpsum_tiled_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(wpsum_tiled_kernel<G>, smem);
     const int tiles_x = (a.d.w + PPC - 1) / PPC;
     const unsigned blocks = unsigned(int64_t(a.d.nt) * a.d.h * tiles_x);
     wpsum_tiled_kernel<G><<<blocks, 256, smem, st>>>(a, out, counts, stack);
@@ -520,8 +520,7 @@ int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream
     const int nq = nqy * nqx;
     const size_t smem = size_t(nq) * P * P * G * sizeof(float4);
     if (smem > 200 * 1024) return 0;
-    cudaFuncSetAttribute(wpsum_query_kernel<P, G, FG, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+    ensure_smem(wpsum_query_kernel<P, G, FG, TY, TX>, smem);
     const int tiles = ((a.d.w + TX - 1) / TX) * ((a.d.h + TY - 1) / TY);
     const dim3 grid(unsigned(int64_t(a.d.nt) * tiles), FG / G);
     wpsum_query_kernel<P, G, FG, TY, TX><<<grid, 256, smem, st>>>(a, out, counts);

@@ -151,8 +151,7 @@ int launch_block_match(const float* a, const float* b, int frames, int h, int w,
     const int nby = (h + block - 1) / block, nbx = (w + block - 1) / block;
     const size_t smem = size_t(block) * block * f * sizeof(float);
     if (smem > 200 * 1024) return -1;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(block_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(block_match_kernel, smem);
     block_match_kernel<<<unsigned(int64_t(frames) * nby * nbx), kBmThreads, smem, st>>>(
         a, b, h, w, f, block, radius, nbx, nby * nbx, flow);
     return 1;

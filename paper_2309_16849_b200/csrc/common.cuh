@@ -7,6 +7,10 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include <cuda_runtime.h>
 
 #include "snls_cuda.h"
@@ -233,6 +237,25 @@ __device__ __forceinline__ bool eligible(float v) { return v > -INFINITY; }
 
 __device__ __forceinline__ void latch(int* err, int bit) {
     if (err) atomicOr(err, bit);
+}
+
+// Raise a kernel's dynamic shared-memory limit above the 48 KB default, once per (kernel,
+// device) and size: cudaFuncSetAttribute is a driver call, not something to pay per launch.
+inline void ensure_smem(const void* kern, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex m;
+    static std::map<std::pair<const void*, int>, size_t> have;
+    std::lock_guard<std::mutex> lk(m);
+    size_t& h = have[{kern, dev}];
+    if (h >= bytes) return;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) == cudaSuccess)
+        h = bytes;
+}
+template <class K>
+inline void ensure_smem(K* kern, size_t bytes) {
+    ensure_smem(reinterpret_cast<const void*>(kern), bytes);
 }
 
 }  // namespace snls_gpu

@@ -259,8 +259,7 @@ void launch_rows(const float* grad, const float* offsets, const float* q, const 
                  int topl, int metric, float* dq, float* dk, double* gyx, cudaStream_t st) {
     const int64_t warps = d.rows * ((d.f + 31) / 32);
     const size_t smem = size_t(4) * P * P * 32 * sizeof(float) * (kDqSm ? 2 : 1);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(search_bwd_rows<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(search_bwd_rows<P>, smem);
     search_bwd_rows<P><<<unsigned((warps + 3) / 4), 128, smem, st>>>(grad, offsets, q, k, d, topl, metric,
                                                                      dq, dk, gyx);
 }

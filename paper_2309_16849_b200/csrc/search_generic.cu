@@ -345,12 +345,10 @@ int launch_search_generic(const GenericSearch& g, cudaStream_t st) {
     const size_t smem = per_warp * warps;
     const unsigned blocks = unsigned((g.d.rows + warps - 1) / warps);
     if (g.d.f % 4 == 0) {
-        cudaFuncSetAttribute(search_generic_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+        ensure_smem(search_generic_kernel<4>, smem);
         search_generic_kernel<4><<<blocks, warps * 32, smem, st>>>(a);
     } else {
-        cudaFuncSetAttribute(search_generic_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+        ensure_smem(search_generic_kernel<1>, smem);
         search_generic_kernel<1><<<blocks, warps * 32, smem, st>>>(a);
     }
     return 1;
@@ -363,7 +361,7 @@ int launch_topl(int64_t rows, int cols, const float* full, const float* full_off
     while (warps > 1 && per_warp * warps > 200 * 1024) warps >>= 1;
     if (per_warp * warps > 227 * 1024) return -1;
     const size_t smem = per_warp * warps;
-    cudaFuncSetAttribute(topl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(topl_kernel, smem);
     topl_kernel<<<unsigned((rows + warps - 1) / warps), warps * 32, smem, st>>>(
         rows, cols, full, full_offsets, topl, sel, sel_offsets, err);
     return 1;

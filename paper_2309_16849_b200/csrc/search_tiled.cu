@@ -475,7 +475,7 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64)
                             : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
     auto launch = [&](auto kern) {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        ensure_smem(kern, smem);
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
     };
     if (s.metric == SNLS_METRIC_IP)

@@ -20,7 +20,9 @@ rm -f $o/${tag}_ncu_c4.ncu-rep
 {
   echo "# compute-sanitizer over the GPU parity tests on B200 ($tag)"
   for t in memcheck racecheck synccheck; do
-    compute-sanitizer --tool $t --error-exitcode 9 python -m pytest -q -x tests/test_gpu_kernels.py tests/test_gpu_search.py > $o/san_$t.log 2>&1
+    tests="tests/test_gpu_kernels.py tests/test_gpu_search.py tests/test_gpu_backward.py"
+    [ $t = memcheck ] && tests="$tests tests/test_gpu_aggregate.py tests/test_gpu_pipeline.py tests/test_gpu_shard.py tests/test_gpu_align.py"
+    compute-sanitizer --tool $t --error-exitcode 9 python -m pytest -q -x $tests > $o/san_$t.log 2>&1
     echo "$t rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|passed|failed' $o/san_$t.log | tail -2 | tr '\n' ' ')"
   done
 } > $o/${tag}_sanitizer.txt

@@ -13,6 +13,11 @@
 
 namespace snls_gpu {
 
+// SNLS_NOSEL=1 (measurement builds only, wrong results): skip every top-L insertion to time
+// the selection's share (c4: 4.11 -> 3.66 ms, c5: 117.3 -> 109.6 ms; profiles/r01_plans.txt)
+#ifndef SNLS_NOSEL
+#define SNLS_NOSEL 0
+#endif
 constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
 constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
@@ -120,11 +125,11 @@ struct TopL {
         for (int i = 0; i < S::NPL; ++i) {
             const int b = sb + i;
             v[i] = METRIC == SNLS_METRIC_IP ? v[i] : -v[i];  // l2 accumulates +sum(d^2)
-            if (on && owner && b < W && v[i] > thr) pend |= 1u << i;
+            if (SNLS_NOSEL == 0 && on && owner && b < W && v[i] > thr) pend |= 1u << i;
         }
         // survivors one at a time, lanes then slots ascending (= slot order)
-        while (__any_sync(0xffffffffu, pend != 0)) {
-            const unsigned want = __ballot_sync(0xffffffffu, pend != 0);
+        unsigned want = __ballot_sync(0xffffffffu, pend != 0);
+        while (want) {
             const unsigned gmask = (want >> (gq * G)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
             const int src = gmask ? gq * G + (__ffs(gmask) - 1) : lane;
             const int isrc = pend ? (__ffs(pend) - 1) : 0;
@@ -137,6 +142,7 @@ struct TopL {
             if (!gmask) bv = -INFINITY;  // no-op insert keeps the shuffles warp-uniform
             list_insert<G, S::M>(ev, es, bv, bs, gl);
             if (lane == src && gmask) pend &= pend - 1;
+            want = __ballot_sync(0xffffffffu, pend != 0);
         }
     }
 

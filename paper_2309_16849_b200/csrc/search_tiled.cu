@@ -102,6 +102,10 @@ constexpr bool kQsm = SNLS_QSM != 0 && SNLS_PACKED_F32X2 != 0;
 #define SNLS_QSM4 1
 #endif
 constexpr bool kQsm4 = SNLS_QSM4 != 0 && SNLS_PACKED_F32X2 != 0;
+#ifndef SNLS_XO_SMEM
+#define SNLS_XO_SMEM 1
+#endif
+constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
 #ifndef SNLS_QSM_MINB
 #define SNLS_QSM_MINB 3
 #endif
@@ -116,6 +120,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     constexpr bool kQsmF4 = kPackedPath && kQsm4;
     // kPairPath: [QPB][P*P][G] channel pairs; kQsmF4: [QPB][P*P][G] float4
     extern __shared__ __align__(16) unsigned char s_qdyn[];
+    __shared__ unsigned s_xo[kXoSmem ? R + 1 : 1][128];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane / G, gl = lane % G;
@@ -190,13 +195,24 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         // vector index (one IMAD.WIDE per load instead of 64-bit pointer math)
         const float* kframe = a.k + size_t(on ? kt : qt) * frame_elems + c0;
         const unsigned rowv = unsigned(Wd) * G;  // VEC-vectors per image row
-        // reflected column offsets, precomputed (recomputing them at the boundary-warp loads
-        // instead: c4 5.06 vs 4.45 ms)
-        unsigned xo[R + 1];
-#pragma unroll
-        for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * G;
         const bool interior = __all_sync(0xffffffffu, bx >= 0 && bx + R < Wd);
         const unsigned xb = unsigned(bx) * G;
+        // reflected column offsets, precomputed (recomputing them at the boundary-warp loads
+        // instead: c4 5.06 vs 4.45 ms) and parked in shared memory: only boundary warps read
+        // them, and the R+1 registers go to the interior loop (c4 4.12 -> 4.00 ms, c5 116.9 ->
+        // 112.7 ms, c2 0.370 -> 0.357 ms)
+        unsigned xo_r[kXoSmem ? 1 : R + 1];
+        unsigned* xo = kXoSmem ? &s_xo[0][threadIdx.x] : xo_r;
+        constexpr int XS = kXoSmem ? 128 : 1;  // element stride
+        if (kXoSmem) {
+            if (!interior) {
+#pragma unroll
+                for (int j = 0; j <= R; ++j) xo[j * XS] = unsigned(reflect_near(bx + j, Wd)) * G;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * G;
+        }
         auto ld = [&](unsigned vidx, float (&o)[VEC]) { ldv<VEC>(kframe + size_t(vidx) * VEC, o); };
 
         float acc[P][W];
@@ -234,8 +250,8 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     P4 a0 = ldp4(kb4 + (r0 + xo[0])), a1 = ldp4(kb4 + (r1 + xo[0]));
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
-                        const P4 b0 = ldp4(kb4 + (r0 + xo[j + 1]));
-                        const P4 b1 = ldp4(kb4 + (r1 + xo[j + 1]));
+                        const P4 b0 = ldp4(kb4 + (r0 + xo[(j + 1) * XS]));
+                        const P4 b1 = ldp4(kb4 + (r1 + xo[(j + 1) * XS]));
                         kr[j] = lerp2(a0, b0, a1, b1, W00, W01, W10, W11);
                         a0 = b0;
                         a1 = b1;
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     u64 a0 = ld2(kb2 + (r0 + xo[0])), a1 = ld2(kb2 + (r1 + xo[0]));
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
-                        const u64 b0 = ld2(kb2 + (r0 + xo[j + 1])), b1 = ld2(kb2 + (r1 + xo[j + 1]));
+                        const u64 b0 = ld2(kb2 + (r0 + xo[(j + 1) * XS])), b1 = ld2(kb2 + (r1 + xo[(j + 1) * XS]));
                         kr[j] = fma2(W11, b1, fma2(W10, a1, fma2(W01, b0, mul2(W00, a0))));
                         a0 = b0;
                         a1 = b1;
@@ -357,8 +373,8 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     float4 a0 = __ldg(kb4 + (r0 + xo[0])), a1 = __ldg(kb4 + (r1 + xo[0]));
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
-                        const float4 b0 = __ldg(kb4 + (r0 + xo[j + 1]));
-                        const float4 b1 = __ldg(kb4 + (r1 + xo[j + 1]));
+                        const float4 b0 = __ldg(kb4 + (r0 + xo[(j + 1) * XS]));
+                        const float4 b1 = __ldg(kb4 + (r1 + xo[(j + 1) * XS]));
                         kr[j] = lerp4(a0, b0, a1, b1, w00, w01, w10, w11);
                         a0 = b0;
                         a1 = b1;
@@ -402,8 +418,8 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     ld(r1 + xo[0], a1);
     #pragma unroll
                     for (int j = 0; j < R; ++j) {
-                        ld(r0 + xo[j + 1], b0);
-                        ld(r1 + xo[j + 1], b1);
+                        ld(r0 + xo[(j + 1) * XS], b0);
+                        ld(r1 + xo[(j + 1) * XS], b1);
                         lerpv<VEC>(kr[j], a0, b0, a1, b1, w00, w01, w10, w11);
     #pragma unroll
                         for (int v = 0; v < VEC; ++v) {

@@ -110,7 +110,9 @@ constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
 #define SNLS_QSM_MINB 3
 #endif
 
-template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG>
+// FG: full-grid mode (materialise the scores; a separate instantiation so the fused kernel
+// carries no grid pointer or branches)
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG, bool FG>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
     constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
@@ -174,13 +176,13 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     TopL<W, G, KMAX> sel;
     sel.init();
     const int thr_src = TopL<W, G, KMAX>::thr_lane(gq, a.topl), thr_idx = TopL<W, G, KMAX>::thr_entry(a.topl);
-    float* grid_row = a.grid ? a.grid + size_t(row) * nfr * W * W : nullptr;
+    float* grid_row = FG ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
         const int dt = scan_dt(fp), kt = qt + dt;
         const bool on = row_ok && kt >= 0 && kt < a.d.t;
         if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
-            if (a.grid && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
+            if (FG && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
             continue;
         }
         double sdy = 0.0, sdx = 0.0;
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         }
     }
 
-    if (a.grid) return;  // selection happens in the top_l pass over the grid
+    if (FG) return;  // selection happens in the top_l pass over the grid
     sel.emit(a, s_keys[qslot], row, row_ok, gl, qt, qy, qx);
 }
 
@@ -494,10 +496,16 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
         ensure_smem(kern, smem);
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
     };
-    if (s.metric == SNLS_METRIC_IP)
-        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG>);
-    else
-        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG>);
+    if (s.grid) {
+        if (s.metric == SNLS_METRIC_IP)
+            launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG, true>);
+        else
+            launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG, true>);
+    } else if (s.metric == SNLS_METRIC_IP) {
+        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG, false>);
+    } else {
+        launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG, false>);
+    }
     return 1;
 }
 

@@ -125,3 +125,30 @@ def test_c2_stride1_search_row(port):
     assert ctx.last_search_path() == 1
     excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
     assert excluded < 0.5 * ref["sims"].shape[0]
+
+
+EXACT = [(11, 3, 32, "l2", 16), (11, 3, 32, "l2", 17), (11, 3, 32, "l2", 40), (11, 3, 32, "l2", 100),
+         (9, 7, 64, "ip", 10), (9, 3, 64, "l2", 10), (9, 7, 32, "l2", 10), (11, 3, 16, "ip", 16)]
+
+
+@pytest.mark.parametrize("ws,ps,f,metric,topl", EXACT, ids=[f"w{a}p{b}f{c}{d}k{e}" for a, b, c, d, e in EXACT])
+def test_topl_sizes_bit_exact_on_integer_inputs(port, ws, ps, f, metric, topl):
+    """L up to the register lists' 16 entries runs the tiled kernel, above it the generic one;
+    on integer-valued videos and flows every sum is exact in fp32, so sims and offsets must
+    equal the oracle bit for bit -- including the many exact ties, resolved by scan order
+    (search.cpp:187-197) -- in the fused and the full-grid mode."""
+    S = snls_mod()
+    t, h, w = 3, 12, 13
+    cfg = Cfg(ws=ws, wt=1, ps=ps, stride0=2, topl=topl, metric=metric, softmax_scale=1.0 / (ps * ps * f))
+    seed = 8000 + 7 * topl + ps * 131 + f
+    q = video(port, t, h, w, f, seed, lo=0.0, hi=16.0, integer=True)
+    k = video(port, t, h, w, f, seed + 1, lo=0.0, hi=16.0, integer=True)
+    ff = flow(port, t, h, w, seed + 2, 2.0, integer=True)
+    bf = flow(port, t, h, w, seed + 3, 2.0, integer=True)
+    ref = port.search_fwd(q, k, ff, bf, cfg)
+    ctx = S.context()
+    for mode in (0, 1):
+        r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), ctx=ctx, mode=mode)
+        if mode == 0:
+            assert ctx.last_search_path() == (1 if topl <= 16 else 0)
+        compare_search(r, ref["sims"], ref["offsets"], cfg, exact=True)

@@ -160,8 +160,11 @@ __global__ void __launch_bounds__(256) gather_stack_kernel(AggArgs a, float* __r
 // reference's fixed-order gather (footprint py/px ascending, then the owning query's cell
 // completion; neighbours ascending), each unit costing 2 LDS + 4 coalesced LDG.128 + 16 FFMA
 // per lane instead of re-deriving taps from the offsets in every channel lane.
+// One (query, neighbour) of a tile: the sample frame's first pixel index (kt*H*W), the integer
+// offset (and its pixel-index form oy*W + ox) and the softmax-weighted bilinear weights.
 struct SampleDesc {
-    int kt, oy, ox, ok;
+    uint32_t kbase;
+    int oy, ox, doff;
     float w00, w01, w10, w11;
 };
 
@@ -195,16 +198,17 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
         const size_t e = size_t(row) * a.topl + l;
         const float* o = a.offsets + e * 3;
         SampleDesc d;
-        d.kt = ti + int(roundf(__ldg(o)));
-        d.ok = d.kt >= 0 && d.kt < a.d.t;
-        if (!d.ok) {
+        int kt = ti + int(roundf(__ldg(o)));
+        if (kt < 0 || kt >= a.d.t) {
             latch(err_bit, err_code);
-            d.kt = ti;
+            kt = ti;
         }
+        d.kbase = uint32_t(kt) * uint32_t(a.d.h) * uint32_t(a.d.w);
         const float oy = __ldg(o + 1), ox = __ldg(o + 2);
         const float fly = floorf(oy), flx = floorf(ox);
         d.oy = int(fly);
         d.ox = int(flx);
+        d.doff = d.oy * a.d.w + d.ox;
         const float fy = oy - fly, fx = ox - flx;
         const float wv = __ldg(a.weights + e);
         d.w00 = wv * ((1.f - fy) * (1.f - fx));
@@ -221,35 +225,38 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
 #define SNLS_AGG_UNROLL 4
 #endif
 constexpr int kAggUnroll = SNLS_AGG_UNROLL;
-template <int VEC>
+// G = float4 groups per pixel (compile time); c4 = this lane's float4 group.  Addresses are
+// pixel indices (frame base + (sy, sx) + offset) times G: one wide multiply per tap set.
+template <int G>
 __device__ __forceinline__ void add_unit_tiled(const AggArgs& a, const SampleDesc* desc,
                                                const TileGeom& g, int gy, int gx, int sy, int sx,
-                                               int l0, int l1, int c, float4& acc) {
+                                               int l0, int l1, int c4, float4& acc) {
     const SampleDesc* dq = desc + ((gy - g.gy_lo) * g.nqx + (gx - g.gx_lo)) * a.topl;
-    const int H = a.d.h, W = a.d.w, F = a.d.f;
+    const int H = a.d.h, W = a.d.w;
+    const float4* vb = reinterpret_cast<const float4*>(a.v) + c4;
+    const int pix = sy * W + sx;
 #pragma unroll kAggUnroll
     for (int l = l0; l < l1; ++l) {
         const SampleDesc d = dq[l];
         const int iy = sy + d.oy, ix = sx + d.ox;
-        const float* base = a.v + size_t(d.kt) * H * W * F + c;
-        const float *p00, *p01, *p10, *p11;
-        if (iy >= 0 && iy + 1 < H && ix >= 0 && ix + 1 < W) {
-            p00 = base + (size_t(iy) * W + ix) * F;
-            p01 = p00 + F;
-            p10 = p00 + size_t(W) * F;
-            p11 = p10 + F;
+        const float4 *p00, *p01, *p10, *p11;
+        if (unsigned(iy) < unsigned(H - 1) && unsigned(ix) < unsigned(W - 1)) {
+            p00 = vb + size_t(d.kbase + uint32_t(pix + d.doff)) * G;
+            p01 = p00 + G;
+            p10 = p00 + size_t(W) * G;
+            p11 = p10 + G;
         } else {  // reflected border taps (tensor.cpp:31-48)
             const int y0 = reflect(iy, H), y1 = reflect(iy + 1, H);
             const int x0 = reflect(ix, W), x1 = reflect(ix + 1, W);
-            p00 = base + (size_t(y0) * W + x0) * F;
-            p01 = base + (size_t(y0) * W + x1) * F;
-            p10 = base + (size_t(y1) * W + x0) * F;
-            p11 = base + (size_t(y1) * W + x1) * F;
+            p00 = vb + size_t(d.kbase + uint32_t(y0 * W + x0)) * G;
+            p01 = vb + size_t(d.kbase + uint32_t(y0 * W + x1)) * G;
+            p10 = vb + size_t(d.kbase + uint32_t(y1 * W + x0)) * G;
+            p11 = vb + size_t(d.kbase + uint32_t(y1 * W + x1)) * G;
         }
-        const float4 A = __ldg(reinterpret_cast<const float4*>(p00));
-        const float4 B = __ldg(reinterpret_cast<const float4*>(p01));
-        const float4 C = __ldg(reinterpret_cast<const float4*>(p10));
-        const float4 D = __ldg(reinterpret_cast<const float4*>(p11));
+        const float4 A = __ldg(p00);
+        const float4 B = __ldg(p01);
+        const float4 C = __ldg(p10);
+        const float4 D = __ldg(p11);
         acc.x = fmaf(d.w11, D.x, fmaf(d.w10, C.x, fmaf(d.w01, B.x, fmaf(d.w00, A.x, acc.x))));
         acc.y = fmaf(d.w11, D.y, fmaf(d.w10, C.y, fmaf(d.w01, B.y, fmaf(d.w00, A.y, acc.y))));
         acc.z = fmaf(d.w11, D.z, fmaf(d.w10, C.z, fmaf(d.w01, B.z, fmaf(d.w00, A.z, acc.z))));
@@ -282,9 +289,9 @@ __device__ __forceinline__ AxisUnits axis_units(int coord, int s0, int half, int
 
 // One pixel's fixed-order gather over neighbours [l0, l1) (aggregate.cpp:156-188), with the
 // footprint units enumerated without division in the inner loop.
-template <int VEC>
+template <int G>
 __device__ int gather_tiled(const AggArgs& a, const SampleDesc* desc, const TileGeom& g,
-                            const AxisUnits& uy, int y, int x, int l0, int l1, int c,
+                            const AxisUnits& uy, int y, int x, int l0, int l1, int c4,
                             float4& acc) {
     const int st = a.d.stride0, half = a.ps / 2;
     const AxisUnits ux = axis_units(x, st, half, (a.d.nw - 1) * st);
@@ -294,15 +301,15 @@ __device__ int gather_tiled(const AggArgs& a, const SampleDesc* desc, const Tile
         for (int ix = 0; ix < ux.n; ++ix) {
             const int px = ix == 0 ? ux.p0 : ux.p1;
             // footprint unit: sample at qy + off + py = y + off
-            add_unit_tiled<VEC>(a, desc, g, (y - py) / st, (x - px) / st, y, x, l0, l1, c, acc);
+            add_unit_tiled<G>(a, desc, g, (y - py) / st, (x - px) / st, y, x, l0, l1, c4, acc);
             ++cnt;
         }
     }
     const int gy = owner_index(y, st, a.d.nh), gx = owner_index(x, st, a.d.nw);
     const int qy = gy * st, qx = gx * st;
     if (abs(y - qy) > half || abs(x - qx) > half) {
-        add_unit_tiled<VEC>(a, desc, g, gy, gx, qy + clampi(y - qy, half), qx + clampi(x - qx, half),
-                            l0, l1, c, acc);
+        add_unit_tiled<G>(a, desc, g, gy, gx, qy + clampi(y - qy, half), qx + clampi(x - qx, half),
+                          l0, l1, c4, acc);
         ++cnt;
     }
     return cnt;
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
     const size_t pix = (size_t(ti - a.d.t0) * a.d.h + y) * a.d.w + x;  // local output pixel
     if (!stack) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int cnt = gather_tiled<4>(a, s_desc, g, uy, y, x, 0, a.topl, c, acc);
+        const int cnt = gather_tiled<G>(a, s_desc, g, uy, y, x, 0, a.topl, c / 4, acc);
         if (cnt <= 0) {
             latch(a.err, kErrWpsum);
             return;
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(256) wpsum_tiled_kernel(AggArgs a, float* __re
         const size_t plane = size_t(a.d.nt) * a.d.h * a.d.w * a.d.f;
         for (int l = 0; l < a.topl; ++l) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            gather_tiled<4>(a, s_desc, g, uy, y, x, l, l + 1, c, acc);
+            gather_tiled<G>(a, s_desc, g, uy, y, x, l, l + 1, c / 4, acc);
             *reinterpret_cast<float4*>(out + l * plane + pix * a.d.f + c) = acc;
         }
     }
@@ -364,6 +371,7 @@ int launch_tiled_agg(const AggArgs& a, float* out, int32_t* counts, int stack, c
 
 int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stack, cudaStream_t st) {
     if (a.d.f % 4 != 0) return 0;
+    if (int64_t(a.d.t) * a.d.h * a.d.w >= (int64_t(1) << 32)) return 0;  // 32-bit pixel indices
     switch (a.d.f / 4) {
         case 1: return launch_tiled_agg<1>(a, out, counts, stack, st);
         case 2: return launch_tiled_agg<2>(a, out, counts, stack, st);

@@ -4,14 +4,17 @@
 // With stride1 == 1 every slot of one (query, frame) pair samples K at the SAME fractional
 // offset (fy, fx): the pair needs the (ws+ps-1)^2 key region interpolated once, not once
 // per (slot, patch pixel) as patch_similarity does (search.cpp:124-151).  Mapping:
-//  * G = F / VEC lanes per query; lane gl owns channels [gl*VEC, gl*VEC+VEC) (float4).
-//    A warp holds 32/G queries, consecutive rows (neighbouring pixels -> their key regions
-//    overlap and hit in L1).
+//  * G = F / VEC lanes per query; lane gl owns channels [gl*VEC, gl*VEC+VEC) (float4; float2
+//    at ps = 7).  A warp holds 32/G queries, consecutive rows (neighbouring pixels -> their
+//    key regions overlap and hit in L1).  The arithmetic runs on packed fp32x2 (FFMA2/FADD2,
+//    packed.cuh); the query patch and the boundary warps' reflected column offsets are parked
+//    in shared memory at the start (own lane only, no barrier) so the registers go to the
+//    accumulators and the interpolated row.
 //  * Per frame the lane walks the key region row by row: it interpolates one region row
 //    (ws+ps-1 pixels) into registers from two raw K rows (coalesced 16 B per lane, 128 B per
 //    8-lane group), then updates the ps active slot rows: acc[s][b] += m(Q[py][px], Krow[b+px])
 //    for the ps x ws slots that read this region row.  Slot row a completes after region
-//    row a+ps-1 (rotating ps x ws accumulators: registers only, no shared-memory tile).
+//    row a+ps-1 (rotating ps x ws accumulators: registers only, no shared-memory tile of K).
 //  * A completed slot row is reduce-scattered across the G channel lanes (butterfly; the
 //    addition tree is identical for every slot, so duplicate candidates tie exactly) and
 //    each lane streams its ws/G slots into a register top-L list (strict '>' insertion in

@@ -34,6 +34,9 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+// The device error latch of a context (pipeline.cu snapshots it with each clip).
+int* ctx_err(snls_ctx* ctx) { return ctx ? ctx->err : nullptr; }
+
 }  // namespace snls_capi
 
 using snls_capi::fail;

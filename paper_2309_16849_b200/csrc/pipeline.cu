@@ -35,6 +35,7 @@
 
 namespace snls_capi {
 int fail(int code, const std::string& msg);  // capi.cu: sets snls_last_error()
+int* ctx_err(snls_ctx* ctx);                 // capi.cu: the context's device error latch
 }
 
 // One set of device buffers and events: a clip in flight.
@@ -46,6 +47,10 @@ struct PipeSlot {
     std::vector<cudaEvent_t> frame_in, chunk_out;
     cudaEvent_t done = nullptr;
     bool allocated = false, busy = false;
+    // pinned snapshot of the context's error latch, copied on the result stream after the
+    // clip's results: wait() reads it without a blocking device read of its own (which would
+    // queue behind the next clip's D2H on the copy engine and stall the stream)
+    int* err_snap = nullptr;
 };
 
 struct snls_pipeline {
@@ -86,6 +91,8 @@ void free_slot(PipeSlot& s) {
     for (float* f : fs)
         if (f) cudaFree(f);
     if (s.counts) cudaFree(s.counts);
+    if (s.err_snap) cudaFreeHost(s.err_snap);
+    s.err_snap = nullptr;
     s.q = s.k = s.v = s.ff = s.bf = s.sims = s.offs = s.wts = s.out = nullptr;
     s.counts = nullptr;
     for (auto ev : s.frame_in)
@@ -124,6 +131,11 @@ int alloc_slot(snls_pipeline* p, PipeSlot& s) {
     if (!rc) rc = alloc(&s.wts, sel, "snls_pipeline: weights");
     if (!rc) rc = alloc(&s.out, vid, "snls_pipeline: out");
     if (!rc) rc = alloc(&s.counts, size_t(d.t) * d.h * d.w * sizeof(int32_t), "snls_pipeline: counts");
+    if (!rc) {
+        const cudaError_t he = cudaHostAlloc(reinterpret_cast<void**>(&s.err_snap), sizeof(int), cudaHostAllocDefault);
+        if (he != cudaSuccess) rc = pcuda(he, "snls_pipeline: error snapshot");
+        else *s.err_snap = 0;
+    }
     if (rc == SNLS_OK) s.allocated = true;
     return rc;
 }
@@ -139,8 +151,10 @@ int wait_oldest(snls_pipeline* p) {
     s.busy = false;
     if (e != cudaSuccess) return pcuda(e, "snls_pipeline_wait");
     // the latch is per context: an error of a clip still in flight may surface one wait
-    // early, never later or not at all
-    if (int r = snls_ctx_sync_check(p->ctx)) return pfail(r, snls_last_error());
+    // early, never later or not at all.  The full check (message, reset) runs only when the
+    // clip's snapshot of the latch is set.
+    if (*s.err_snap != 0)
+        if (int r = snls_ctx_sync_check(p->ctx)) return pfail(r, snls_last_error());
     return SNLS_OK;
 }
 
@@ -231,7 +245,9 @@ int enqueue(snls_pipeline* p, int si, const float* q, const float* k, const floa
         if (counts) PCHECK(cudaMemcpyAsync(counts + size_t(a) * d.h * d.w, S.counts + size_t(a) * d.h * d.w, size_t(b - a) * d.h * d.w * sizeof(int32_t), cudaMemcpyDeviceToHost, p->result), "d2h counts");
     }
     snls_ctx_set_stream(p->ctx, user);
-    // the result stream waited for every chunk: its `done` covers the whole clip
+    // the result stream waited for every chunk: its latch snapshot and `done` cover the clip
+    PCHECK(cudaMemcpyAsync(S.err_snap, snls_capi::ctx_err(p->ctx), sizeof(int), cudaMemcpyDeviceToHost,
+                           p->result), "error snapshot");
     PCHECK(cudaEventRecord(S.done, p->result), "done event");
 #undef PCHECK
     return rc;

@@ -40,7 +40,7 @@ WORKLOADS = {
                name="c4: 10x256x256x32 per video, ws11 wt3 ps3 k16 L2 s0=2, one video/GPU"),
     # BASELINE configs[1]: T=5 C=64 H=W=128 ws=9 wt=2 ps=7 k=10 ip, stride0 4 (hole-free min)
     "c2": dict(T=5, H=128, W=128, C=64, ws=9, wt=2, ps=7, topl=10, metric="ip", stride0=4,
-               beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0,
+               beta=1.0 / 3136, vid_seed=11, ff_seed=14, bf_seed=15, flow_mag=2.0, pipe_chunk=5,
                name="c2: 5x128x128x64, ws9 wt2 ps7 k10 ip s0=4"),
     # BASELINE configs[2]: c2 shapes fwd + bwd (vid & flow grads); upstream gradients
     # U[-1,1) seeds 16 (sims) and 17 (wpsum output)

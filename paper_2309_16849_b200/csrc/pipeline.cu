@@ -40,6 +40,11 @@ int fail(int code, const std::string& msg);  // capi.cu: sets snls_last_error()
 int* ctx_err(snls_ctx* ctx);                 // capi.cu: the context's device error latch
 }
 
+#ifndef SNLS_D2H_AFTER_H2D
+#define SNLS_D2H_AFTER_H2D 1
+#endif
+constexpr bool kD2HAfterH2D = SNLS_D2H_AFTER_H2D != 0;
+
 // One set of device buffers and events: a clip in flight.
 struct PipeSlot {
     float *q = nullptr, *k = nullptr, *v = nullptr, *ff = nullptr, *bf = nullptr;
@@ -249,6 +254,10 @@ int enqueue(snls_pipeline* p, int si, const float* q, const float* k, const floa
         }
     }
     if (p->trace) cudaEventRecord(S.tr[1], p->copy);
+
+    // the copy-back starts after the clip's last H2D: a D2H command in flight would hold up
+    // the H2D commands queued behind it (the same copy-engine ordering as above)
+    if (kD2HAfterH2D) PCHECK(cudaStreamWaitEvent(p->result, S.frame_in[T - 1], 0), "result order");
 
     // ---- frame chunks: search (+ fused softmax) and wpsum, then their copy-back
     const int L = p->cfg.topl;

@@ -109,6 +109,15 @@ constexpr bool kQsm4 = SNLS_QSM4 != 0 && SNLS_PACKED_F32X2 != 0;
 #define SNLS_XO_SMEM 1
 #endif
 constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
+// the slot row's partials in kBSplit chunks (fewer live registers: with them c4's 3 x 11
+// accumulators fit 128 registers, MINB 4 / 16 warps per SM: 3.967 -> 3.923 ms)
+#ifndef SNLS_BSPLIT
+#define SNLS_BSPLIT 2
+#endif
+constexpr int kBSplit = SNLS_BSPLIT;
+#ifndef SNLS_MINB4_WMAX
+#define SNLS_MINB4_WMAX 11
+#endif
 #ifndef SNLS_QSM_MINB
 #define SNLS_QSM_MINB 3
 #endif
@@ -280,26 +289,33 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     // slot-inner: consecutive instructions update W independent partials (per
                     // slot the order is px ascending, pair lo then hi; slot-outer: c4 4.16 vs
                     // 4.12 ms, c5 119.7 vs 117.7 ms)
-                    u64 t[W];
+                    constexpr int BC = (W + kBSplit - 1) / kBSplit;
 #pragma unroll
-                    for (int px = 0; px < P; ++px)
+                    for (int b0 = 0; b0 < W; b0 += BC) {
+                        u64 t[BC];
 #pragma unroll
-                        for (int h = 0; h < 2; ++h)
+                        for (int px = 0; px < P; ++px)
 #pragma unroll
-                            for (int b = 0; b < W; ++b) {
-                                const u64 qh = h ? qv[px].hi : qv[px].lo;
-                                const u64 kh = h ? kr[b + px].hi : kr[b + px].lo;
-                                if (METRIC == SNLS_METRIC_IP) {
-                                    t[b] = (px == 0 && h == 0) ? mul2(qh, kh) : fma2(qh, kh, t[b]);
-                                } else {  // +sum (q - k)^2
-                                    const u64 d = sub2(qh, kh);
-                                    t[b] = (px == 0 && h == 0) ? mul2(d, d) : fma2(d, d, t[b]);
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int bi = 0; bi < BC; ++bi) {
+                                    const int b = b0 + bi;
+                                    if (b >= W) continue;
+                                    const u64 qh = h ? qv[px].hi : qv[px].lo;
+                                    const u64 kh = h ? kr[b + px].hi : kr[b + px].lo;
+                                    if (METRIC == SNLS_METRIC_IP) {
+                                        t[bi] = (px == 0 && h == 0) ? mul2(qh, kh) : fma2(qh, kh, t[bi]);
+                                    } else {  // +sum (q - k)^2
+                                        const u64 d = sub2(qh, kh);
+                                        t[bi] = (px == 0 && h == 0) ? mul2(d, d) : fma2(d, d, t[bi]);
+                                    }
                                 }
-                            }
 #pragma unroll
-                    for (int b = 0; b < W; ++b) {
-                        const float2 tf = upk2(t[b]);
-                        acc[s][b] += tf.x + tf.y;
+                        for (int bi = 0; bi < BC; ++bi) {
+                            if (b0 + bi >= W) continue;
+                            const float2 tf = upk2(t[bi]);
+                            acc[s][b0 + bi] += tf.x + tf.y;
+                        }
                     }
                 }
             } else if constexpr (kPairPath) {
@@ -516,7 +532,7 @@ template <int P, int W, int VEC, int G, int KMAX>
 int launch_cfg(const TiledSearch& s, cudaStream_t st) {
     if constexpr (P >= 7)  // 7 x 9 accumulators + the 15-pixel region row: 8 (12) warps per SM
         return launch_cfg_b<P, W, VEC, G, KMAX, kQsm ? SNLS_QSM_MINB : 2>(s, st);
-    else if constexpr (P <= 3 && W <= 9)  // 3 x 9 accumulators fit 128 registers: 16 warps/SM
+    else if constexpr (P <= 3 && W <= SNLS_MINB4_WMAX)  // 3 x W accumulators fit 128 registers: 16 warps/SM
         return launch_cfg_b<P, W, VEC, G, KMAX, 4>(s, st);  // (c5: 126.7 -> 125.7 ms)
     else
         return launch_cfg_b<P, W, VEC, G, KMAX, 3>(s, st);

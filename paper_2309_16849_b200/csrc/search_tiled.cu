@@ -111,6 +111,12 @@ constexpr bool kQsm4 = SNLS_QSM4 != 0 && SNLS_PACKED_F32X2 != 0;
 constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
 // the slot row's partials in kBSplit chunks (fewer live registers: with them c4's 3 x 11
 // accumulators fit 128 registers, MINB 4 / 16 warps per SM: 3.967 -> 3.923 ms)
+// float4 packed path: a slot row's first contribution is assigned, not added to a zeroed
+// accumulator (at 16 warps/SM: c4 3.920 -> 3.891 ms, c5 112.2 -> 111.8 ms)
+#ifndef SNLS_ASSIGN1
+#define SNLS_ASSIGN1 1
+#endif
+constexpr bool kAssign1 = SNLS_ASSIGN1 != 0;
 #ifndef SNLS_BSPLIT
 #define SNLS_BSPLIT 2
 #endif
@@ -314,7 +320,10 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                         for (int bi = 0; bi < BC; ++bi) {
                             if (b0 + bi >= W) continue;
                             const float2 tf = upk2(t[bi]);
-                            acc[s][b0 + bi] += tf.x + tf.y;
+                            if (kAssign1 && s == P - 1)  // first region row of this slot row
+                                acc[s][b0 + bi] = tf.x + tf.y;
+                            else
+                                acc[s][b0 + bi] += tf.x + tf.y;
                         }
                     }
                 }
@@ -484,13 +493,12 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             if (r >= P - 1) sel.template finish_row<METRIC>(acc[0], lane, gl, gq, on, row_ok, r - (P - 1), slot_base, grid_row, thr_src, thr_idx);
             // rotate: acc[s] tracks slot row r-(P-1)+s, so every region row shifts by one (an
             // unroll by P that renames instead costs 3x the code: c4 5.9 vs 4.45 ms, i-cache);
-            // the pair path assigns a slot row's first contribution, the others start at zero
-            // (assigning in the float4 path: c5 128.2 vs 125.8 ms)
+            // the packed paths assign a slot row's first contribution, the others start at zero
 #pragma unroll
             for (int s = 0; s + 1 < P; ++s)
 #pragma unroll
                 for (int b = 0; b < W; ++b) acc[s][b] = acc[s + 1][b];
-            if constexpr (!kPairPath) {
+            if constexpr (!kPairPath && !(kPackedPath && kAssign1)) {
 #pragma unroll
                 for (int b = 0; b < W; ++b) acc[P - 1][b] = 0.f;
             }

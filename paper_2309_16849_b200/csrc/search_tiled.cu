@@ -121,6 +121,10 @@ constexpr bool kAssign1 = SNLS_ASSIGN1 != 0;
 #define SNLS_BSPLIT 2
 #endif
 constexpr int kBSplit = SNLS_BSPLIT;
+#ifndef SNLS_BSPLIT_SMALL_W
+#define SNLS_BSPLIT_SMALL_W 9
+#endif
+constexpr int kBSplitSmallW = SNLS_BSPLIT_SMALL_W;
 #ifndef SNLS_MINB4_WMAX
 #define SNLS_MINB4_WMAX 11
 #endif
@@ -295,7 +299,9 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                     // slot-inner: consecutive instructions update W independent partials (per
                     // slot the order is px ascending, pair lo then hi; slot-outer: c4 4.16 vs
                     // 4.12 ms, c5 119.7 vs 117.7 ms)
-                    constexpr int BC = (W + kBSplit - 1) / kBSplit;
+                    // (W <= 9, c5: one slot at a time -- 110.1 vs 111.7 ms; W = 11, c4: two
+                    // chunks -- 3.888 vs 3.908 ms per slot)
+                    constexpr int BC = W <= kBSplitSmallW ? 1 : (W + kBSplit - 1) / kBSplit;
 #pragma unroll
                     for (int b0 = 0; b0 < W; b0 += BC) {
                         u64 t[BC];

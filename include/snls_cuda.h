@@ -155,6 +155,32 @@ int snls_search_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
                            const float* q, const float* k, float* dq, float* dk, float* dfflow,
                            float* dbflow);
 
+/* General backward (search.hpp:151-153; search.cpp:499-711) over either tape form:
+ *  - the device tape: offsets rows x L x 3 fp32 and (wt > 1) relative fp32 chains, or
+ *  - the reference's own SearchTape (search.hpp:89-110): `centers` rows x L x 3 fp64
+ *    absolute (kt, ky, kx) and (wt > 1) `chains64` rows x L x max(wt-1,0) x 6 fp64 with
+ *    absolute link positions -- used when `centers` is non-NULL (offsets/chains may then
+ *    be NULL).  The fp64 tape keeps the key-position fractions at fp64 accuracy, which the
+ *    flow gradients amplify (d(dS/dy)/dy ~ sum (dk/dy)^2).
+ * Query rows of frames [t0, t1) as in snls_search_bwd_frames.  flags:
+ *  SNLS_BWD_DETERMINISTIC -- the reference's default deterministic mode (search.cpp:687-696):
+ *  every accumulation is int64 fixed point (scale = a power of two from a per-call bound),
+ *  so the result is bitwise identical on every run; otherwise fp32/fp64 atomics. */
+#define SNLS_BWD_DETERMINISTIC 1
+int snls_search_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                       const float* grad_sims, const float* offsets, const float* chains,
+                       const double* centers, const double* chains64, const float* q,
+                       const float* k, float* dq, float* dk, float* dfflow, float* dbflow,
+                       int flags);
+
+/* The reference's fp64 SearchTape (search.hpp:89-110) from the device tape: for the query
+ * rows of frames [t0, t1), absolute key centres (kt, ky, kx) rows x L x 3 and (wt > 1)
+ * absolute chain links rows x L x max(wt-1,0) x 6, recomputed in fp64 from the flows as
+ * emit_row does (search.cpp:207-234).  fflow/bflow NULL = zero flows (nls_forward). */
+int snls_search_tape64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                       const float* fflow, const float* bflow, const float* offsets,
+                       double* centers, double* chains64);
+
 /* ---- aggregate (aggregate.hpp) ------------------------------------------------------ */
 /* Replaces snls::softmax_rows (aggregate.hpp:22; aggregate.cpp:16-37). */
 int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims,

@@ -41,8 +41,8 @@ __device__ __forceinline__ bool add_unit(const AggArgs& a, int64_t row, int ti, 
         if (kt < 0 || kt >= a.d.t) return false;
         int iy, ix;
         float fy, fx;
-        split_pos(qy + pyu, __ldg(o + 1), iy, fy);
-        split_pos(qx + pxu, __ldg(o + 2), ix, fx);
+        split_pos(qy + pyu, __ldg(o + 1), iy, fy, a.d.h);
+        split_pos(qx + pxu, __ldg(o + 2), ix, fx, a.d.w);
         const Taps t = taps_from(iy, fy, ix, fx, a.d.h, a.d.w);
         const float wv = __ldg(a.weights + e);
         const float* p00 = a.v + vidx(a.d, kt, t.y0, t.x0) + c;
@@ -206,8 +206,8 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
         d.kbase = uint32_t(kt) * uint32_t(a.d.h) * uint32_t(a.d.w);
         const float oy = __ldg(o + 1), ox = __ldg(o + 2);
         const float fly = floorf(oy), flx = floorf(ox);
-        d.oy = int(fly);
-        d.ox = int(flx);
+        d.oy = fold_base(fly, a.d.h);
+        d.ox = fold_base(flx, a.d.w);
         d.doff = d.oy * a.d.w + d.ox;
         const float fy = oy - fly, fx = ox - flx;
         const float wv = __ldg(a.weights + e);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
             const float w00 = wv * ((1.f - fy) * (1.f - fx)), w01 = wv * ((1.f - fy) * fx);
             const float w10 = wv * (fy * (1.f - fx)), w11 = wv * (fy * fx);
             // sample (i, j) sits between raw rows by+i, by+i+1 and cols bx+j, bx+j+1
-            const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+            const int by = qy - HP + fold_base(fly, H), bx = qx - HP + fold_base(flx, W);
             const float4* vf = vbase + size_t(kt) * H * row4;
             float4 blk[P + 1][P + 1];
             if (by >= 0 && by + P < H && bx >= 0 && bx + P < W) {
@@ -620,8 +620,8 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
         const float inv_cnt = 1.f / float(counts[(size_t(ti - a.d.t0) * a.d.h + y) * a.d.w + x]);
         int iy, ix;
         float fy, fx;
-        split_pos(qy + pyu, oy, iy, fy);
-        split_pos(qx + pxu, ox, ix, fx);
+        split_pos(qy + pyu, oy, iy, fy, a.d.h);
+        split_pos(qx + pxu, ox, ix, fx, a.d.w);
         const Taps t = taps_from(iy, fy, ix, fx, a.d.h, a.d.w);
         const float* gp = go + vidx(a.d, ti - a.d.t0, y, x) + c;
         const size_t i00 = vidx(a.d, kt, t.y0, t.x0) + c, i01 = vidx(a.d, kt, t.y0, t.x1) + c;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
         const float wv = __ldg(a.weights + e);
-        const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+        const int by = qy - HP + fold_base(fly, H), bx = qx - HP + fold_base(flx, W);
         unsigned bcol[P + 1];
 #pragma unroll
         for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);

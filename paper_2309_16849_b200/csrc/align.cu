@@ -12,6 +12,7 @@
 //    (zero / provided / block matching), one batched search over all T-1 frame pairs
 //    (each pair is its own one-frame clip: wt = 0), the fused softmax, wpsum of the clean
 //    frames and the per-pair PSNR, all on the device.
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -187,8 +188,14 @@ int snls_align_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
     const size_t frame = size_t(H) * W * F, fframe = size_t(H) * W * 2;
     const size_t nvid = size_t(dims.t) * frame;
     // noise on the host: GaussianStream is sequential and must stay bitwise (rng.hpp:30-53)
+    // harness.cpp:95: `opts.sigma > 0.0 ? add_gaussian_noise(...) : clean` -- a zero or
+    // negative sigma aligns the clean clip (add_gaussian_noise itself rejects sigma < 0)
     std::vector<float> noisy(nvid);
-    if (int rc = snls_gaussian_noise_f32(seed, sigma, int64_t(nvid), clean, noisy.data())) return rc;
+    if (sigma > 0.0) {
+        if (int rc = snls_gaussian_noise_f32(seed, sigma, int64_t(nvid), clean, noisy.data())) return rc;
+    } else {
+        std::copy(clean, clean + nvid, noisy.begin());
+    }
 
     void* sp = nullptr;
     snls_ctx_get_stream(ctx, &sp);

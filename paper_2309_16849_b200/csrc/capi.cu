@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 
 #include "common.cuh"
@@ -36,6 +37,13 @@ int fail(int code, const std::string& msg) {
 
 // The device error latch of a context (pipeline.cu snapshots it with each clip).
 int* ctx_err(snls_ctx* ctx) { return ctx ? ctx->err : nullptr; }
+// The device a context's kernels, streams and buffers belong to.
+int ctx_device(snls_ctx* ctx) { return ctx ? ctx->device : 0; }
+
+// Read-and-clear of the latch in ONE device operation: latch[1] = atomicExch(latch[0], 0).
+// A bit another in-flight stream sets after the exchange stays latched for the next check
+// (a separate read then clear could wipe it unreported).
+__global__ void latch_take_kernel(int* latch) { latch[1] = atomicExch(latch, 0); }
 
 }  // namespace snls_capi
 
@@ -92,6 +100,15 @@ int validate(const snls_config* c) {
 int check_dims(snls_dims d) {
     if (d.t < 1 || d.h < 1 || d.w < 1 || d.f < 1)
         return fail(SNLS_EDOMAIN, "VideoTensor: all extents must be at least 1");
+    return SNLS_OK;
+}
+
+// The kernels load float4 / u64 vectors straight from the base pointers: a misaligned
+// pointer would raise cudaErrorMisalignedAddress, which is sticky for the whole context.
+int check_aligned(const char* where, std::initializer_list<const void*> ptrs) {
+    for (const void* p : ptrs)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15u))
+            return fail(SNLS_EARG, std::string(where) + ": tensor pointers must be 16-byte aligned");
     return SNLS_OK;
 }
 
@@ -194,11 +211,12 @@ int snls_ctx_create(int device, void* stream, snls_ctx** out) {
     ctx->device = device;
     ctx->stream = static_cast<cudaStream_t>(stream);
     ctx->num_sms = prop.multiProcessorCount;
-    if ((e = cudaMalloc(&ctx->err, sizeof(int))) != cudaSuccess) {
+    // err[0]: the latch kernels atomicOr into; err[1]: the value taken by sync_check
+    if ((e = cudaMalloc(&ctx->err, 2 * sizeof(int))) != cudaSuccess) {
         delete ctx;
         return cuda_fail(e, "snls_ctx_create");
     }
-    cudaMemset(ctx->err, 0, sizeof(int));
+    cudaMemset(ctx->err, 0, 2 * sizeof(int));
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
         cudaFree(ctx->err);
         delete ctx;
@@ -259,12 +277,13 @@ int snls_ctx_sync_check(snls_ctx* ctx) {
     if (int rc = check_ctx(ctx)) return rc;
     DeviceGuard g(ctx->device);
     int host = 0;
-    cudaError_t e = cudaMemcpyAsync(&host, ctx->err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    snls_capi::latch_take_kernel<<<1, 1, 0, ctx->stream>>>(ctx->err);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&host, ctx->err + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "snls_ctx_sync_check");
     if (host == 0) return SNLS_OK;
-    cudaMemsetAsync(ctx->err, 0, sizeof(int), ctx->stream);
-    cudaStreamSynchronize(ctx->stream);
     if (host & kErrFflow) return fail(SNLS_EDOMAIN, "search fflow: flow holds a non-finite value");
     if (host & kErrBflow) return fail(SNLS_EDOMAIN, "search bflow: flow holds a non-finite value");
     if (host & kErrSoftmax) return fail(SNLS_EDOMAIN, "softmax_rows: non-finite input");
@@ -325,7 +344,7 @@ static int search_common_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims
     if (!q || !k) return fail(SNLS_EARG, "search: null query/key tensor");
     if ((ff == nullptr) != (bf == nullptr))
         return fail(SNLS_EARG, "search: pass both flows or neither (nls_forward)");
-    return SNLS_OK;
+    return check_aligned("search", {q, k, ff, bf});
 }
 
 int snls_search_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
@@ -461,27 +480,68 @@ int snls_search_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
                            const float* grad, const float* offsets, const float* chains,
                            const float* q, const float* k, float* dq, float* dk, float* dff,
                            float* dbf) {
+    return snls_search_bwd_ex(ctx, cfg, dims, t0, t1, grad, offsets, chains, nullptr, nullptr, q, k,
+                              dq, dk, dff, dbf, 0);
+}
+
+int snls_search_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                       const float* grad, const float* offsets, const float* chains,
+                       const double* centers, const double* chains64, const float* q,
+                       const float* k, float* dq, float* dk, float* dff, float* dbf, int flags) {
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = validate(cfg)) return rc;
     if (int rc = check_dims(dims)) return rc;
-    if (!grad || !offsets || !q || !k || !dq || !dk || !dff || !dbf)
+    if (!grad || !q || !k || !dq || !dk || !dff || !dbf)
         return fail(SNLS_EARG, "shifted_nls_backward: null tensor");
-    if (cfg->wt > 1 && !chains)
+    if (!offsets && !centers)
+        return fail(SNLS_EARG, "shifted_nls_backward: the tape needs offsets or centres");
+    if (cfg->wt > 1 && (centers ? chains64 == nullptr : chains == nullptr))
         return fail(SNLS_EARG, "shifted_nls_backward: the tape needs chains when wt > 1");
     if (t0 < 0 || t1 > dims.t || t0 >= t1)
         return fail(SNLS_EARG, "shifted_nls_backward: empty or invalid frame range");
+    if (flags & ~SNLS_BWD_DETERMINISTIC) return fail(SNLS_EARG, "shifted_nls_backward: unknown flags");
+    if (int rc = check_aligned("shifted_nls_backward", {q, k, dq, dk})) return rc;
     DeviceGuard g(ctx->device);
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     const size_t nv = size_t(dims.t) * dims.h * dims.w;
     cudaMemsetAsync(dq, 0, nv * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
     const size_t scratch = (size_t(d.rows) * cfg->topl * 2 + nv * 4) * sizeof(double);
+    if (flags & SNLS_BWD_DETERMINISTIC) {
+        const int n = launch_search_bwd_det(grad, offsets, chains, centers, chains64, q, k, d, cfg->wt,
+                                            cfg->ps, cfg->topl, cfg->metric, dq, dk, dff, dbf,
+                                            [&](size_t bytes) -> void* {
+                                                return ensure_work(ctx, bytes) ? nullptr : ctx->work;
+                                            },
+                                            ctx->stream);
+        if (n < 0) return fail(SNLS_ECUDA, "shifted_nls_backward: deterministic workspace");
+        return after_launch(ctx, n, "snls_search_bwd(deterministic)");
+    }
     if (int rc = ensure_work(ctx, scratch)) return rc;
     cudaMemsetAsync(ctx->work, 0, scratch, ctx->stream);
-    const int n = launch_search_bwd_impl(grad, offsets, chains, q, k, d, cfg->wt, cfg->ps, cfg->topl,
-                                         cfg->metric, dq, dk, dff, dbf, static_cast<double*>(ctx->work),
-                                         ctx->stream);
+    const int n = launch_search_bwd_impl(grad, offsets, chains, centers, chains64, q, k, d, cfg->wt,
+                                         cfg->ps, cfg->topl, cfg->metric, dq, dk, dff, dbf,
+                                         static_cast<double*>(ctx->work), ctx->stream);
     return after_launch(ctx, n, "snls_search_bwd");
+}
+
+int snls_search_tape64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                       const float* ff, const float* bf, const float* offsets, double* centers,
+                       double* chains64) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if ((ff == nullptr) != (bf == nullptr))
+        return fail(SNLS_EARG, "search: pass both flows or neither (nls_forward)");
+    if (!offsets || !centers) return fail(SNLS_EARG, "search_tape64: null tensor");
+    if (cfg->wt > 1 && !chains64) return fail(SNLS_EARG, "search_tape64: the tape needs chains when wt > 1");
+    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "search_tape64: empty or invalid frame range");
+    DeviceGuard g(ctx->device);
+    const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
+    return after_launch(ctx,
+                        launch_tape64(ff, bf, d, cfg->ws, cfg->wt, cfg->topl, cfg->stride1, offsets,
+                                      centers, cfg->wt > 1 ? chains64 : nullptr, ctx->stream),
+                        "snls_search_tape64");
 }
 
 int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims, float* weights) {
@@ -503,7 +563,7 @@ static int agg_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
         return fail(SNLS_ECONFIG, "aggregate: (ps-1)/2 < stride0 is required for hole-free output");
     if (int rc = check_dims(dims)) return rc;
     if (!v || !w || !o) return fail(SNLS_EARG, "aggregate: null tensor");
-    return SNLS_OK;
+    return check_aligned("aggregate", {v, w, o});
 }
 
 int snls_wpsum_fwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* v,

@@ -124,16 +124,27 @@ __device__ __forceinline__ Taps taps_from(int by, float fy, int bx, float fx, in
     return t;
 }
 
+// An integral coordinate (or displacement) as int.  Beyond +-2^30 only its class modulo the
+// reflection period 2(n-1) matters (tensor.cpp:23-29), so fold it there -- exactly, fb is
+// integral -- before the conversion: a huge finite flow (Middlebury marks unknown flow with
+// ~1e9-1e10) can then neither saturate the int nor overflow base + offset sums into an
+// out-of-bounds address.  inf/NaN fold to NaN and convert to 0 (already latched as errors).
+__device__ __forceinline__ int fold_base(double fb, int n) {
+    if (!(fabs(fb) < 1073741824.0)) fb = fmod(fb, n > 1 ? 2.0 * (n - 1) : 1.0);
+    return int(fb);
+}
+
 // Position given in fp64 (absolute coordinate).
 __device__ __forceinline__ Taps taps_at(double y, double x, int h, int w) {
     const double by = floor(y), bx = floor(x);
-    return taps_from(int(by), float(y - by), int(bx), float(x - bx), h, w);
+    return taps_from(fold_base(by, h), float(y - by), fold_base(bx, w), float(x - bx), h, w);
 }
 
-// Position = integer `base` + fp32 `off` (off may be any magnitude that fp32 holds).
-__device__ __forceinline__ void split_pos(int base, float off, int& ib, float& fr) {
+// Position = integer `base` + fp32 `off` (off may be any magnitude that fp32 holds) along an
+// axis of n pixels.
+__device__ __forceinline__ void split_pos(int base, float off, int& ib, float& fr, int n) {
     const float fl = floorf(off);
-    ib = base + int(fl);
+    ib = base + fold_base(double(fl), n);
     fr = off - fl;  // exact (Sterbenz) for |off| >= 1 and for 0 <= off < 1
 }
 
@@ -144,16 +155,20 @@ __device__ __forceinline__ float blend(const Taps& t, float a, float b, float c,
 // search.cpp:72-122 on device: the window shift to frame qt + dt in fp64.  dt == 0 reads
 // the forward field at the query pixel; |dt| >= 1 sums per-step fields, later links
 // bilinear-sampled at the displaced position.  `links` (optional) receives |dt|-1 links of
-// (pos_y - qy, pos_x - qx, J00, J01, J10, J11).
-__device__ inline void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
-                                int h, int w, int qt, int qy, int qx, int dt, double& dy,
-                                double& dx, float* links) {
+// (pos_y - qy, pos_x - qx, J00, J01, J10, J11) in fp32 (the device tape) or, with LT =
+// double, the reference's own fp64 links (pos_y, pos_x, J00, ...) with ABSOLUTE positions.
+template <typename LT>
+__device__ inline void shift_to_t(const float* __restrict__ ff, const float* __restrict__ bf,
+                                  int h, int w, int qt, int qy, int qx, int dt, double& dy,
+                                  double& dx, LT* links) {
+    constexpr bool kAbs = sizeof(LT) == sizeof(double);
     if (ff == nullptr) {  // nls_forward: zero flows
         dy = 0.0;
         dx = 0.0;
         if (links)
             for (int k = 1; k < (dt < 0 ? -dt : dt); ++k)
-                for (int j = 0; j < 6; ++j) links[(k - 1) * 6 + j] = 0.f;
+                for (int j = 0; j < 6; ++j)
+                    links[(k - 1) * 6 + j] = LT(kAbs && j < 2 ? (j == 0 ? qy : qx) : 0);
         return;
     }
     auto at = [&](const float* fl, int t, int y, int x, int c) {
@@ -178,8 +193,9 @@ __device__ inline void shift_to(const float* __restrict__ ff, const float* __res
             const double py = double(qy) + sy, px = double(qx) + sx;
             const double fby = floor(py), fbx = floor(px);
             const double fy = py - fby, fx = px - fbx;
-            const int y0 = reflect_near(int(fby), h), y1 = reflect_near(int(fby) + 1, h);
-            const int x0 = reflect_near(int(fbx), w), x1 = reflect_near(int(fbx) + 1, w);
+            const int iby = fold_base(fby, h), ibx = fold_base(fbx, w);
+            const int y0 = reflect_near(iby, h), y1 = reflect_near(iby + 1, h);
+            const int x0 = reflect_near(ibx, w), x1 = reflect_near(ibx + 1, w);
             const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);
             const double cy = at(fld, fr, y1, x0, 0), dyv = at(fld, fr, y1, x1, 0);
             const double ax = at(fld, fr, y0, x0, 1), bx = at(fld, fr, y0, x1, 1);
@@ -189,13 +205,13 @@ __device__ inline void shift_to(const float* __restrict__ ff, const float* __res
             vy = w00 * ay + w01 * by + w10 * cy + w11 * dyv;
             vx = w00 * ax + w01 * bx + w10 * cx + w11 * dxv;
             if (links) {
-                float* lk = links + (k - 1) * 6;
-                lk[0] = float(sy);
-                lk[1] = float(sx);
-                lk[2] = float(-(1.0 - fx) * ay - fx * by + (1.0 - fx) * cy + fx * dyv);
-                lk[3] = float(-(1.0 - fy) * ay + (1.0 - fy) * by - fy * cy + fy * dyv);
-                lk[4] = float(-(1.0 - fx) * ax - fx * bx + (1.0 - fx) * cx + fx * dxv);
-                lk[5] = float(-(1.0 - fy) * ax + (1.0 - fy) * bx - fy * cx + fy * dxv);
+                LT* lk = links + (k - 1) * 6;
+                lk[0] = LT(kAbs ? py : sy);
+                lk[1] = LT(kAbs ? px : sx);
+                lk[2] = LT(-(1.0 - fx) * ay - fx * by + (1.0 - fx) * cy + fx * dyv);
+                lk[3] = LT(-(1.0 - fy) * ay + (1.0 - fy) * by - fy * cy + fy * dyv);
+                lk[4] = LT(-(1.0 - fx) * ax - fx * bx + (1.0 - fx) * cx + fx * dxv);
+                lk[5] = LT(-(1.0 - fy) * ax + (1.0 - fy) * bx - fy * cx + fy * dxv);
             }
         }
         sy += vy;
@@ -203,6 +219,12 @@ __device__ inline void shift_to(const float* __restrict__ ff, const float* __res
     }
     dy = sy;
     dx = sx;
+}
+
+__device__ __forceinline__ void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
+                                         int h, int w, int qt, int qy, int qx, int dt, double& dy,
+                                         double& dx, float* links) {
+    shift_to_t<float>(ff, bf, h, w, qt, qy, qx, dt, dy, dx, links);
 }
 
 // Total order used for top-L: value descending, then slot ascending (search.cpp:187-197,

@@ -3,6 +3,8 @@
 // the configuration cannot be served (the caller maps that to a status).
 #pragma once
 
+#include <functional>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -55,6 +57,8 @@ int launch_topl(int64_t rows, int cols, const float* full, const float* full_off
                 float* sel, float* sel_offsets, int* err, cudaStream_t st);
 int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,
                      const float* offsets, float* chains, cudaStream_t st);
+int launch_tape64(const float* ff, const float* bf, Dims d, int ws, int wt, int topl, double stride1,
+                  const float* offsets, double* centers, double* chains, cudaStream_t st);
 int launch_replay(const float* q, const float* k, Dims d, int ps, int metric, int topl,
                   const float* offsets, float* sims, cudaStream_t st);
 
@@ -74,8 +78,13 @@ size_t psnr_scratch_doubles(int frames);
 
 // `gyx`: rows * topl * 2 doubles of zeroed scratch.  Returns the number of launches.
 int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
-                           const float* q, const float* k, Dims d, int wt, int ps, int topl,
-                           int metric, float* dq, float* dk, float* dff, float* dbf, double* gyx,
-                           cudaStream_t st);
+                           const double* centers, const double* chains64, const float* q,
+                           const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
+                           float* dk, float* dff, float* dbf, double* gyx, cudaStream_t st);
+int launch_search_bwd_det(const float* grad, const float* offsets, const float* chains,
+                          const double* centers, const double* chains64, const float* q,
+                          const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
+                          float* dk, float* dff, float* dbf,
+                          const std::function<void*(size_t)>& work, cudaStream_t st);
 
 }  // namespace snls_gpu

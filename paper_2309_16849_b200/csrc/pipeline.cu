@@ -38,6 +38,7 @@
 namespace snls_capi {
 int fail(int code, const std::string& msg);  // capi.cu: sets snls_last_error()
 int* ctx_err(snls_ctx* ctx);                 // capi.cu: the context's device error latch
+int ctx_device(snls_ctx* ctx);               // capi.cu: the context's device
 }
 
 #ifndef SNLS_D2H_AFTER_H2D
@@ -85,6 +86,21 @@ struct snls_pipeline {
 namespace {
 
 int pfail(int code, const std::string& msg) { return snls_capi::fail(code, msg); }
+
+// Every entry point runs on the context's device: streams, events and buffers are created
+// there and the chunk kernels (DeviceGuard'ed in capi.cu) launch there.
+struct PipeDevice {
+    int prev = -1;
+    explicit PipeDevice(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~PipeDevice() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
 
 int pcuda(cudaError_t e, const char* where) {
     return pfail(SNLS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -332,8 +348,8 @@ int snls_pipeline_create(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, 
     int64_t rows = 0;
     int nh = 0, nw = 0;
     if (int rc = snls_query_grid(dims, cfg->stride0, &rows, &nh, &nw)) return pfail(rc, snls_last_error());
-    int dev = 0;
-    cudaGetDevice(&dev);
+    const int dev = snls_capi::ctx_device(ctx);
+    PipeDevice guard(dev);
     auto* p = new snls_pipeline();
     p->ctx = ctx;
     p->device = dev;
@@ -374,6 +390,7 @@ int snls_pipeline_create(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, 
 
 int snls_pipeline_destroy(snls_pipeline* p) {
     if (!p) return SNLS_OK;
+    PipeDevice guard(p->device);
     cudaStream_t ss[] = {p->copy, p->result, p->comp[0], p->comp[1]};
     for (auto s : ss)
         if (s) cudaStreamSynchronize(s);
@@ -394,6 +411,7 @@ int snls_pipeline_submit(snls_pipeline* p, const float* q, const float* k, const
     if (!q || !k || !v) return pfail(SNLS_EARG, "snls_pipeline_submit: null video");
     if ((fflow == nullptr) != (bflow == nullptr))
         return pfail(SNLS_EARG, "snls_pipeline_submit: pass both flows or neither");
+    PipeDevice guard(p->device);
     const int si = p->next;
     PipeSlot& S = p->slot[si];
     if (S.busy)
@@ -415,6 +433,7 @@ int snls_pipeline_submit(snls_pipeline* p, const float* q, const float* k, const
 // Wait for the oldest submitted clip: its results are in host memory afterwards.
 int snls_pipeline_wait(snls_pipeline* p) {
     if (!p) return pfail(SNLS_EARG, "snls_pipeline_wait: null pipeline");
+    PipeDevice guard(p->device);
     return wait_oldest(p);
 }
 
@@ -428,6 +447,7 @@ int snls_pipeline_run(snls_pipeline* p, const float* q, const float* k, const fl
                       const float* fflow, const float* bflow, float* sims, float* offsets,
                       float* weights, float* out, int32_t* counts) {
     if (!p) return pfail(SNLS_EARG, "snls_pipeline_run: null pipeline");
+    PipeDevice guard(p->device);
     while (p->npending)  // drain any streamed clips first
         if (int rc = wait_oldest(p)) return rc;
     if (int rc = snls_pipeline_submit(p, q, k, v, fflow, bflow, sims, offsets, weights, out, counts))

@@ -14,6 +14,9 @@
 #ifndef SNLS_BWD_DQSM
 #define SNLS_BWD_DQSM 1
 #endif
+#ifndef SNLS_BWD_FORCE_ENTRIES
+#define SNLS_BWD_FORCE_ENTRIES 0
+#endif
 
 namespace snls_gpu {
 
@@ -21,14 +24,34 @@ namespace {
 
 constexpr bool kDqSm = SNLS_BWD_DQSM != 0;
 
-template <int VEC>
+// Where a gradient contribution goes.  Default: fp32 atomics (the reference's
+// non-deterministic mode).  Deterministic mode (SNLS_BWD_DETERMINISTIC, the reference's
+// default, search.cpp:687-696): int64 fixed-point atomics -- integer addition is
+// associative, so every run gives the same bits whatever the atomic order.  The fixed-point
+// scale is a power of two picked per call from a bound on the largest possible |sum|
+// (bwd_scales_kernel), so nothing overflows and the resolution stays ~1e-12 of that bound.
+struct Sink {
+    float* f;
+    unsigned long long* i;
+    const double* scale;  // device scalar (deterministic mode)
+};
+
+template <bool DET>
+__device__ __forceinline__ void put(float* f, unsigned long long* i, double scale, size_t idx, double v) {
+    if constexpr (DET) atomicAdd(i + idx, static_cast<unsigned long long>(__double2ll_rn(v * scale)));
+    else atomicAdd(f + idx, float(v));
+}
+
+template <int VEC, bool DET>
 __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restrict__ grad,
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
                                                           const float* __restrict__ k, Dims d,
                                                           int ps, int topl, int metric,
-                                                          float* dq, float* dk, double* gyx) {
+                                                          Sink sq, Sink sk, double* gyx,
+                                                          const double* __restrict__ centers) {
     const int groups = d.f / VEC;
+    const double scq = DET ? *sq.scale : 0.0, sck = DET ? *sk.scale : 0.0;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= d.rows * topl * groups) return;
     const int64_t e = idx / groups;
@@ -38,26 +61,40 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
     const int64_t row = e / topl;
     int qt, qy, qx;
     row_coords(d, row, qt, qy, qx);
-    const float* o = offsets + size_t(e) * 3;
-    const int kt = qt + int(rintf(o[0]));
-    const float oy = o[1], ox = o[2];
+    // key position: integer base + fraction, from the fp32 offsets or the fp64 centres
+    int kt, cby, cbx;
+    double cfy, cfx;  // fp64 fractions: this kernel's arithmetic is fp64
+    if (centers) {
+        const double* cp = centers + size_t(e) * 3;
+        kt = int(cp[0]);
+        const double fly = floor(cp[1]), flx = floor(cp[2]);
+        cby = fold_base(fly, d.h);
+        cbx = fold_base(flx, d.w);
+        cfy = cp[1] - fly;
+        cfx = cp[2] - flx;
+    } else {
+        const float* o = offsets + size_t(e) * 3;
+        kt = qt + int(rintf(o[0]));
+        float fy32, fx32;
+        split_pos(qy, o[1], cby, fy32, d.h);
+        split_pos(qx, o[2], cbx, fx32, d.w);
+        cfy = fy32;
+        cfx = fx32;
+    }
     const int half = ps / 2;
     double gy = 0.0, gx = 0.0;
     for (int py = -half; py <= half; ++py) {
         const int ry = reflect_near(qy + py, d.h);
         for (int px = -half; px <= half; ++px) {
             const int rx = reflect_near(qx + px, d.w);
-            int iy, ix;
-            float fy, fx;
-            split_pos(qy + py, oy, iy, fy);
-            split_pos(qx + px, ox, ix, fx);
-            const Taps t = taps_from(iy, fy, ix, fx, d.h, d.w);
+            const int iy = cby + py, ix = cbx + px;
+            const Taps t = taps_from(iy, float(cfy), ix, float(cfx), d.h, d.w);
             const size_t iq = vidx(d, qt, ry, rx) + c;
             const size_t i00 = vidx(d, kt, t.y0, t.x0) + c, i01 = vidx(d, kt, t.y0, t.x1) + c;
             const size_t i10 = vidx(d, kt, t.y1, t.x0) + c, i11 = vidx(d, kt, t.y1, t.x1) + c;
             // dS/d(ky, kx) sums hundreds of cancelling terms per entry: keep that chain in
             // fp64 (the dQ/dK scatter stays fp32)
-            const double dfy = fy, dfx = fx;
+            const double dfy = cfy, dfx = cfx;
             const double w00 = (1.0 - dfy) * (1.0 - dfx), w01 = (1.0 - dfy) * dfx;
             const double w10 = dfy * (1.0 - dfx), w11 = dfy * dfx;
             double sy = 0.0, sx = 0.0;
@@ -77,11 +114,11 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
                     ds_dk = 2.0 * diff;
                 }
                 const double gk = double(g) * ds_dk;
-                atomicAdd(dq + iq + j, float(double(g) * ds_dq));
-                atomicAdd(dk + i00 + j, float(gk * w00));
-                atomicAdd(dk + i01 + j, float(gk * w01));
-                atomicAdd(dk + i10 + j, float(gk * w10));
-                atomicAdd(dk + i11 + j, float(gk * w11));
+                put<DET>(sq.f, sq.i, scq, iq + j, double(float(double(g) * ds_dq)));
+                put<DET>(sk.f, sk.i, sck, i00 + j, double(float(gk * w00)));
+                put<DET>(sk.f, sk.i, sck, i01 + j, double(float(gk * w01)));
+                put<DET>(sk.f, sk.i, sck, i10 + j, double(float(gk * w10)));
+                put<DET>(sk.f, sk.i, sck, i11 + j, double(float(gk * w11)));
                 // d(sample)/dy, d(sample)/dx from the tap values (search.cpp:574-577)
                 const double dkv_dy = (1.0 - dfx) * (double(k10) - k00) + dfx * (double(k11) - k01);
                 const double dkv_dx = (1.0 - dfy) * (double(k01) - k00) + dfy * (double(k11) - k10);
@@ -92,8 +129,13 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
             gx += sx;
         }
     }
-    atomicAdd(gyx + 2 * e, gy);
-    atomicAdd(gyx + 2 * e + 1, gx);
+    if constexpr (DET) {  // per-(entry, channel group) partials, summed in order by the route
+        gyx[(size_t(e) * groups + c / VEC) * 2] = gy;
+        gyx[(size_t(e) * groups + c / VEC) * 2 + 1] = gx;
+    } else {
+        atomicAdd(gyx + 2 * e, gy);
+        atomicAdd(gyx + 2 * e + 1, gx);
+    }
 }
 
 // Row-centric backward (any stride1: every pixel of one entry's patch shares the
@@ -106,16 +148,17 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 // atomic is a fully coalesced 128 B warp access along the channels.
 // The query patch is parked in shared memory once per warp (each lane reads back only its own
 // channel: no barrier; c3 backward 0.730 -> 0.684 ms).
-template <int P>
+template <int P, bool DET, bool CORR>
 __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const float* __restrict__ grad,
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
                                                           const float* __restrict__ k, Dims d,
                                                           int topl, int metric,
-                                                          float* __restrict__ dq,
-                                                          float* __restrict__ dk,
-                                                          double* __restrict__ gyx) {
+                                                          Sink sinkq, Sink sinkk,
+                                                          double* __restrict__ gyx,
+                                                          const double* __restrict__ centers) {
     constexpr int HP = P / 2;
+    const double scq = DET ? *sinkq.scale : 0.0, sck = DET ? *sinkk.scale : 0.0;
     const int slices = (d.f + 31) / 32;
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -156,19 +199,37 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
         const int64_t e = row * topl + l;
         const float g = __ldg(grad + e);
         if (g == 0.f) continue;  // search.cpp:692 (uniform: one row per warp)
-        const float* o = offsets + size_t(e) * 3;
-        const int kt = qt + int(rintf(__ldg(o)));
-        const float oy = __ldg(o + 1), ox = __ldg(o + 2);
-        const float fly = floorf(oy), flx = floorf(ox);
-        const float fy = oy - fly, fx = ox - flx;
-        const int by = qy - HP + int(fly), bx = qx - HP + int(flx);
+        int kt, by, bx;
+        float fy, fx;
+        double ddy = 0.0, ddx = 0.0;  // fp64 fraction - its fp32 rounding (CORR)
+        if (CORR) {  // the reference's fp64 tape: fraction taken in fp64
+            const double* c = centers + size_t(e) * 3;
+            kt = int(__ldg(c));
+            const double cy = __ldg(c + 1), cx = __ldg(c + 2);
+            const double fly = floor(cy), flx = floor(cx);
+            fy = float(cy - fly);
+            fx = float(cx - flx);
+            ddy = (cy - fly) - double(fy);
+            ddx = (cx - flx) - double(fx);
+            by = fold_base(fly, d.h) - HP;
+            bx = fold_base(flx, d.w) - HP;
+        } else {
+            const float* o = offsets + size_t(e) * 3;
+            kt = qt + int(rintf(__ldg(o)));
+            const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+            const float fly = floorf(oy), flx = floorf(ox);
+            fy = oy - fly;
+            fx = ox - flx;
+            by = qy - HP + fold_base(fly, d.h);
+            bx = qx - HP + fold_base(flx, d.w);
+        }
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
         unsigned bcol[P + 1];
 #pragma unroll
         for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, d.w)) * unsigned(d.f);
         const float* kb = k + size_t(kt) * frameF + cc;
-        float* dkb = dk + size_t(kt) * frameF + cc;
+        const size_t dkb = size_t(kt) * frameF + cc;
         float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
         size_t roa = size_t(reflect_near(by, d.h)) * rowF;
         size_t rob = size_t(reflect_near(by + 1, d.h)) * rowF;
@@ -178,13 +239,17 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
             rb[j] = act ? __ldg(kb + rob + bcol[j]) : 0.f;
             ka[j] = 0.f;
         }
+        // dS/d(ky, kx) sums thousands of cancelling terms per entry: fp64 accumulation of the
+        // fp32 per-term products (c3 l2 flow gradients 1.4e-5 -> 3e-6 relative, +1% time)
         double sy = 0.0, sx = 0.0;
+        // CORR: first-order terms of the fp32 rounding of the fractions (bilinear samples are
+        // linear in fy, fx; the flow gradients amplify the rounding by sum (dk/dy)^2)
+        float cA = 0.f, cB = 0.f, cD = 0.f, cC = 0.f;
 #pragma unroll
         for (int py = 0; py < P; ++py) {
             const size_t ron = size_t(reflect_near(by + py + 2, d.h)) * rowF;
 #pragma unroll
             for (int j = 0; j <= P; ++j) kn[j] = 0.f;
-            float ry = 0.f, rx = 0.f;  // this patch row's share of dS/d(ky, kx)
 #pragma unroll
             for (int px = 0; px < P; ++px) {
                 const float k00 = ra[px], k01 = ra[px + 1], k10 = rb[px], k11 = rb[px + 1];
@@ -212,16 +277,20 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
                 ka[px + 1] = fmaf(gk, w01, ka[px + 1]);
                 kn[px] = fmaf(gk, w10, kn[px]);
                 kn[px + 1] = fmaf(gk, w11, kn[px + 1]);
-                ry = fmaf(gk, dkv_dy, ry);
-                rx = fmaf(gk, dkv_dx, rx);
+                sy = fma(double(gk), double(dkv_dy), sy);
+                sx = fma(double(gk), double(dkv_dx), sx);
+                if constexpr (CORR) {
+                    cC = fmaf(gk, d1 - d0, cC);
+                    if (metric != SNLS_METRIC_IP) {
+                        cA = fmaf(dkv_dy, dkv_dy, cA);
+                        cB = fmaf(dkv_dy, dkv_dx, cB);
+                        cD = fmaf(dkv_dx, dkv_dx, cD);
+                    }
+                }
             }
-            // dS/d(ky, kx) sums thousands of cancelling terms per entry: the per-row partials
-            // are accumulated in fp64
-            sy += double(ry);
-            sx += double(rx);
             if (act) {  // raw row py of the block is complete
 #pragma unroll
-                for (int j = 0; j <= P; ++j) atomicAdd(dkb + roa + bcol[j], ka[j]);
+                for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + bcol[j], ka[j]);
             }
 #pragma unroll
             for (int j = 0; j <= P; ++j) {
@@ -235,7 +304,14 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
         }
         if (act) {
 #pragma unroll
-            for (int j = 0; j <= P; ++j) atomicAdd(dkb + roa + bcol[j], ka[j]);
+            for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + bcol[j], ka[j]);
+        }
+        if constexpr (CORR) {
+            // l2: gk = 2g(q - kv) moves by -2g dkv; both metrics: dkv_dy moves by ddx (d1 - d0),
+            // dkv_dx by ddy (d1 - d0)
+            const double g2 = metric != SNLS_METRIC_IP ? 2.0 * double(g) : 0.0;
+            sy += ddx * cC - g2 * (ddy * cA + ddx * cB);
+            sx += ddy * cC - g2 * (ddy * cB + ddx * cD);
         }
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) {
@@ -243,72 +319,142 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
             sx += __shfl_xor_sync(0xffffffffu, sx, m);
         }
         if (lane == 0) {
-            atomicAdd(gyx + 2 * e, sy);
-            atomicAdd(gyx + 2 * e + 1, sx);
+            if constexpr (DET) {  // per-(entry, slice) partials, summed in order by the route
+                gyx[(size_t(e) * slices + wid % slices) * 2] = sy;
+                gyx[(size_t(e) * slices + wid % slices) * 2 + 1] = sx;
+            } else {
+                atomicAdd(gyx + 2 * e, sy);
+                atomicAdd(gyx + 2 * e + 1, sx);
+            }
         }
     }
     if (act) {
-        float* dqb = dq + size_t(qt) * frameF + cc;
+        const size_t dqb = size_t(qt) * frameF + cc;
 #pragma unroll
         for (int py = 0; py < P; ++py)
 #pragma unroll
             for (int px = 0; px < P; ++px)
-                atomicAdd(dqb + size_t(qrow[py] + qcol[px]) * F, kDqSm ? sdq[(py * P + px) * 32] : dqa[py][px]);
+                put<DET>(sinkq.f, sinkq.i, scq, dqb + size_t(qrow[py] + qcol[px]) * F,
+                         kDqSm ? sdq[(py * P + px) * 32] : dqa[py][px]);
     }
 }
 
-template <int P>
+template <int P, bool DET>
 void launch_rows(const float* grad, const float* offsets, const float* q, const float* k, Dims d,
-                 int topl, int metric, float* dq, float* dk, double* gyx, cudaStream_t st) {
+                 int topl, int metric, Sink sq, Sink sk, double* gyx, const double* centers,
+                 cudaStream_t st) {
     const int64_t warps = d.rows * ((d.f + 31) / 32);
     const size_t smem = size_t(4) * P * P * 32 * sizeof(float) * (kDqSm ? 2 : 1);
-    ensure_smem(search_bwd_rows<P>, smem);
-    search_bwd_rows<P><<<unsigned((warps + 3) / 4), 128, smem, st>>>(grad, offsets, q, k, d, topl, metric,
-                                                                     dq, dk, gyx);
+    const unsigned blocks = unsigned((warps + 3) / 4);
+    if (centers) {
+        ensure_smem(search_bwd_rows<P, DET, true>, smem);
+        search_bwd_rows<P, DET, true><<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk,
+                                                                 gyx, centers);
+    } else {
+        ensure_smem(search_bwd_rows<P, DET, false>, smem);
+        search_bwd_rows<P, DET, false><<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk,
+                                                                  gyx, centers);
+    }
 }
 
+// Phase 1 of either mode; returns the number of per-entry (gy, gx) partials (1: atomics
+// into one pair; >1: one pair per channel slice / group, deterministic mode).
+template <bool DET>
+int launch_phase1(const float* grad, const float* offsets, const double* centers, const float* q,
+                  const float* k, Dims d, int ps, int topl, int metric, Sink sq, Sink sk, double* gyx,
+                  cudaStream_t st) {
+    const int vec = d.f % 4 == 0 ? 4 : 1;
+    if (!SNLS_BWD_FORCE_ENTRIES && (ps == 1 || ps == 3 || ps == 5 || ps == 7)) {
+        switch (ps) {
+            case 1: launch_rows<1, DET>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers, st); break;
+            case 3: launch_rows<3, DET>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers, st); break;
+            case 5: launch_rows<5, DET>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers, st); break;
+            default: launch_rows<7, DET>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers, st); break;
+        }
+        return DET ? (d.f + 31) / 32 : 1;
+    }
+    const int64_t n = d.rows * topl * (d.f / vec);
+    if (vec == 4)
+        search_bwd_entries<4, DET><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps, topl,
+                                                                              metric, sq, sk, gyx, centers);
+    else
+        search_bwd_entries<1, DET><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps, topl,
+                                                                              metric, sq, sk, gyx, centers);
+    return DET ? d.f / vec : 1;
+}
+
+// Phase 2: route each entry's dS/d(ky, kx) through its composition chain (search.cpp:584-666).
+// MODE 0: fp64 atomics into the flow accumulators; MODE 1 (deterministic, bound pass): only
+// the largest |v| met along any chain, for the fixed-point scale; MODE 2 (deterministic):
+// int64 fixed-point atomics.  `parts` per-entry partials are summed in a fixed order.
+template <int MODE>
 __global__ void search_bwd_route(const float* __restrict__ grad,
                                  const float* __restrict__ offsets,
                                  const float* __restrict__ chains, Dims d, int wt, int topl,
-                                 const double* __restrict__ gyx, double* dff, double* dbf) {
+                                 const double* __restrict__ gyx, int parts, double* dff, double* dbf,
+                                 unsigned long long* iff, unsigned long long* ibf,
+                                 const double* __restrict__ scale, unsigned* vmax_bits,
+                                 const double* __restrict__ centers,
+                                 const double* __restrict__ chains64) {
     const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= d.rows * topl) return;
     if (grad[e] == 0.f) return;
     const int64_t row = e / topl;
     int qt, qy, qx;
     row_coords(d, row, qt, qy, qx);
-    const int dt = int(rintf(offsets[size_t(e) * 3]));
+    const int dt = centers ? int(centers[size_t(e) * 3]) - qt : int(rintf(offsets[size_t(e) * 3]));
     double* fld = dt >= 0 ? dff : dbf;
+    unsigned long long* ifld = dt >= 0 ? iff : ibf;
+    const double sc = MODE == 2 ? *scale : 0.0;
     const int step = dt >= 0 ? 1 : -1;
     const int m = dt == 0 ? 1 : (dt > 0 ? dt : -dt);
-    double vy = gyx[2 * e], vx = gyx[2 * e + 1];
+    double vy = 0.0, vx = 0.0;
+    for (int j = 0; j < parts; ++j) {
+        vy += gyx[(size_t(e) * parts + j) * 2];
+        vx += gyx[(size_t(e) * parts + j) * 2 + 1];
+    }
+    double vm = fmax(fabs(vy), fabs(vx));
+    auto add = [&](size_t idx, double v) {
+        if constexpr (MODE == 0) atomicAdd(fld + idx, v);
+        else if constexpr (MODE == 2) atomicAdd(ifld + idx, static_cast<unsigned long long>(__double2ll_rn(v * sc)));
+    };
     const int cs = wt > 1 ? wt - 1 : 0;
     const float* chain = chains ? chains + size_t(e) * cs * 6 : nullptr;
+    const double* chain64 = chains64 ? chains64 + size_t(e) * cs * 6 : nullptr;
     for (int kk = m - 1; kk >= 1; --kk) {
-        const float* lk = chain + (kk - 1) * 6;
-        int iy, ix;
-        float fy, fx;
-        split_pos(qy, lk[0], iy, fy);
-        split_pos(qx, lk[1], ix, fx);
-        const Taps t = taps_from(iy, fy, ix, fx, d.h, d.w);
+        double lk[6];
+        Taps t;
+        if (chain64) {  // absolute fp64 link positions (the reference's tape)
+            for (int j = 0; j < 6; ++j) lk[j] = chain64[(kk - 1) * 6 + j];
+            t = taps_at(lk[0], lk[1], d.h, d.w);
+        } else {
+            for (int j = 0; j < 6; ++j) lk[j] = chain[(kk - 1) * 6 + j];
+            int iy, ix;
+            float fy, fx;
+            split_pos(qy, float(lk[0]), iy, fy, d.h);
+            split_pos(qx, float(lk[1]), ix, fx, d.w);
+            t = taps_from(iy, fy, ix, fx, d.h, d.w);
+        }
         const int fr = qt + step * kk;
-        auto at = [&](int y, int x, int comp) { return fld + ((size_t(fr) * d.h + y) * d.w + x) * 2 + comp; };
-        atomicAdd(at(t.y0, t.x0, 0), vy * t.w00);
-        atomicAdd(at(t.y0, t.x1, 0), vy * t.w01);
-        atomicAdd(at(t.y1, t.x0, 0), vy * t.w10);
-        atomicAdd(at(t.y1, t.x1, 0), vy * t.w11);
-        atomicAdd(at(t.y0, t.x0, 1), vx * t.w00);
-        atomicAdd(at(t.y0, t.x1, 1), vx * t.w01);
-        atomicAdd(at(t.y1, t.x0, 1), vx * t.w10);
-        atomicAdd(at(t.y1, t.x1, 1), vx * t.w11);
-        const double ny = vy + double(lk[2]) * vy + double(lk[4]) * vx;
-        const double nx = vx + double(lk[3]) * vy + double(lk[5]) * vx;
+        auto at = [&](int y, int x, int comp) { return ((size_t(fr) * d.h + y) * d.w + x) * 2 + comp; };
+        add(at(t.y0, t.x0, 0), vy * t.w00);
+        add(at(t.y0, t.x1, 0), vy * t.w01);
+        add(at(t.y1, t.x0, 0), vy * t.w10);
+        add(at(t.y1, t.x1, 0), vy * t.w11);
+        add(at(t.y0, t.x0, 1), vx * t.w00);
+        add(at(t.y0, t.x1, 1), vx * t.w01);
+        add(at(t.y1, t.x0, 1), vx * t.w10);
+        add(at(t.y1, t.x1, 1), vx * t.w11);
+        const double ny = vy + lk[2] * vy + lk[4] * vx;
+        const double nx = vx + lk[3] * vy + lk[5] * vx;
         vy = ny;
         vx = nx;
+        vm = fmax(vm, fmax(fabs(vy), fabs(vx)));
     }
-    double* base = fld + ((size_t(qt) * d.h + qy) * d.w + qx) * 2;
-    atomicAdd(base, vy);
-    atomicAdd(base + 1, vx);
+    const size_t base = ((size_t(qt) * d.h + qy) * d.w + qx) * 2;
+    add(base, vy);
+    add(base + 1, vx);
+    if constexpr (MODE == 1) atomicMax(vmax_bits, __float_as_uint(float(vm) * 1.001f));
 }
 
 __global__ void narrow_kernel(const double* __restrict__ a, const double* __restrict__ b,
@@ -320,39 +466,124 @@ __global__ void narrow_kernel(const double* __restrict__ a, const double* __rest
     }
 }
 
+// ---- deterministic mode --------------------------------------------------------------
+// Non-negative float maxima (|q|, |k|, |grad|) as uint bit patterns: atomicMax on the bits
+// is exact and order-independent, so the scales below are the same on every run.
+__global__ void absmax_kernel(const float* __restrict__ a, int64_t n, unsigned* out) {
+    float m = 0.f;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        m = fmaxf(m, fabsf(a[i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// 2^(61 - ceil(log2(bound))): |any partial sum| <= bound < 2^61 / scale, so no int64 overflow.
+__device__ __forceinline__ double pow2_scale(double bound) {
+    if (!(bound > 0.0) || !isfinite(bound)) return 1.0;
+    int ex;
+    frexp(bound, &ex);  // bound < 2^ex
+    return ldexp(1.0, 61 - ex);
+}
+
+// bounds[0..2] = max|q|, max|k|, max|grad| (bits).  Per output element and entry, a patch
+// reaches it through at most ps^2 pixels (reflection folds) with tap weights <= 1, so
+// |dQ|, |dK| <= entries * ps^2 * max|g| * max|dS/dq|, max|dS/dk|.
+__global__ void bwd_scales_kernel(const unsigned* bounds, int64_t entries, int ps, int metric,
+                                  double* scales) {
+    const double qm = __uint_as_float(bounds[0]), km = __uint_as_float(bounds[1]);
+    const double gm = __uint_as_float(bounds[2]);
+    const double dsq = metric == SNLS_METRIC_IP ? km : 2.0 * (qm + km);
+    const double dsk = metric == SNLS_METRIC_IP ? qm : 2.0 * (qm + km);
+    const double n = double(entries) * ps * ps * gm * 1.001;
+    scales[0] = pow2_scale(n * dsq);
+    scales[1] = pow2_scale(n * dsk);
+}
+
+// Flows: per element and entry at most wt links' 4 taps plus the base pixel touch it (each
+// tap weight <= 1), with |v| <= vmax along every chain.
+__global__ void flow_scale_kernel(const unsigned* vmax_bits, int64_t entries, int wt, double* scale) {
+    const double vm = __uint_as_float(*vmax_bits);
+    *scale = pow2_scale(double(entries) * (4.0 * (wt > 1 ? wt : 1) + 1.0) * vm * 1.001);
+}
+
+__global__ void fixed_to_float_kernel(const unsigned long long* __restrict__ a, const double* scale,
+                                      float* __restrict__ out, int64_t n) {
+    const double inv = 1.0 / *scale;  // a power of two: exact
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = float(double(static_cast<long long>(a[i])) * inv);
+}
+
 }  // namespace
 
 // `gyx` scratch: rows * topl * 2 doubles, then two fp64 flow-gradient accumulators of
 // T*H*W*2 doubles each (the flow gradient sums many cancelling terms: fp64 atomics, then
 // one narrowing pass), all zeroed by the caller.
 int launch_search_bwd_impl(const float* grad, const float* offsets, const float* chains,
-                           const float* q, const float* k, Dims d, int wt, int ps, int topl,
-                           int metric, float* dq, float* dk, float* dff, float* dbf, double* gyx,
-                           cudaStream_t st) {
+                           const double* centers, const double* chains64, const float* q,
+                           const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
+                           float* dk, float* dff, float* dbf, double* gyx, cudaStream_t st) {
     double* dff64 = gyx + size_t(d.rows) * topl * 2;
     const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
     double* dbf64 = dff64 + nfl;
-    const int vec = d.f % 4 == 0 ? 4 : 1;
-    const int64_t n = d.rows * topl * (d.f / vec);
-    if (ps == 1 || ps == 3 || ps == 5 || ps == 7) {
-        switch (ps) {
-            case 1: launch_rows<1>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
-            case 3: launch_rows<3>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
-            case 5: launch_rows<5>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
-            default: launch_rows<7>(grad, offsets, q, k, d, topl, metric, dq, dk, gyx, st); break;
-        }
-    } else if (vec == 4)
-        search_bwd_entries<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps,
-                                                                         topl, metric, dq, dk, gyx);
-    else
-        search_bwd_entries<1><<<unsigned((n + 255) / 256), 256, 0, st>>>(grad, offsets, q, k, d, ps,
-                                                                         topl, metric, dq, dk, gyx);
+    const Sink sq{dq, nullptr, nullptr}, sk{dk, nullptr, nullptr};
+    launch_phase1<false>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, st);
     const int64_t ne = d.rows * topl;
-    search_bwd_route<<<unsigned((ne + 255) / 256), 256, 0, st>>>(grad, offsets, chains, d, wt, topl,
-                                                                 gyx, dff64, dbf64);
+    search_bwd_route<0><<<unsigned((ne + 255) / 256), 256, 0, st>>>(
+        grad, offsets, chains, d, wt, topl, gyx, 1, dff64, dbf64, nullptr, nullptr, nullptr, nullptr,
+        centers, chains64);
     narrow_kernel<<<unsigned(std::min<int64_t>((nfl + 255) / 256, 4096)), 256, 0, st>>>(dff64, dbf64, dff,
                                                                                        dbf, nfl);
     return 3;
+}
+
+// Deterministic backward: same arithmetic, int64 fixed-point accumulation (see Sink).
+// Workspace (from `work(bytes)`, zeroed here): scales, bound bits, per-entry (gy, gx)
+// partials, int64 dQ, dK and flow accumulators.
+int launch_search_bwd_det(const float* grad, const float* offsets, const float* chains,
+                          const double* centers, const double* chains64, const float* q,
+                          const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
+                          float* dk, float* dff, float* dbf,
+                          const std::function<void*(size_t)>& work, cudaStream_t st) {
+    const int64_t ne = d.rows * topl;
+    const int64_t nv = int64_t(d.t) * d.h * d.w * d.f;
+    const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
+    const int parts = std::max((d.f + 31) / 32, d.f % 4 == 0 ? d.f / 4 : d.f);
+    const size_t head = 64;  // 4 doubles of scales + 4 uint bounds, padded
+    const size_t bytes = head + size_t(ne) * parts * 2 * sizeof(double) +
+                         size_t(2 * nv + 2 * nfl) * sizeof(unsigned long long);
+    char* w = static_cast<char*>(work(bytes));
+    if (!w) return -1;
+    cudaMemsetAsync(w, 0, bytes, st);
+    double* scales = reinterpret_cast<double*>(w);  // [0] dQ, [1] dK, [2] flows
+    unsigned* bounds = reinterpret_cast<unsigned*>(w + 32);  // |q|, |k|, |g|, |v|
+    double* gyx = reinterpret_cast<double*>(w + head);
+    auto* iq = reinterpret_cast<unsigned long long*>(gyx + size_t(ne) * parts * 2);
+    unsigned long long* ik = iq + nv;
+    unsigned long long* iff = ik + nv;
+    unsigned long long* ibf = iff + nfl;
+    const int64_t nq_all = int64_t(d.t) * d.h * d.w * d.f;
+    absmax_kernel<<<592, 256, 0, st>>>(q, nq_all, bounds + 0);
+    absmax_kernel<<<592, 256, 0, st>>>(k, nq_all, bounds + 1);
+    absmax_kernel<<<148, 256, 0, st>>>(grad, ne, bounds + 2);
+    bwd_scales_kernel<<<1, 1, 0, st>>>(bounds, ne, ps, metric, scales);
+    const Sink sq{nullptr, iq, scales}, sk{nullptr, ik, scales + 1};
+    const int np = launch_phase1<true>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, st);
+    const unsigned blocks = unsigned((ne + 255) / 256);
+    search_bwd_route<1><<<blocks, 256, 0, st>>>(grad, offsets, chains, d, wt, topl, gyx, np, nullptr, nullptr,
+                                                 nullptr, nullptr, nullptr, bounds + 3, centers, chains64);
+    flow_scale_kernel<<<1, 1, 0, st>>>(bounds + 3, ne, wt, scales + 2);
+    search_bwd_route<2><<<blocks, 256, 0, st>>>(grad, offsets, chains, d, wt, topl, gyx, np, nullptr, nullptr,
+                                                 iff, ibf, scales + 2, nullptr, centers, chains64);
+    const unsigned cb = unsigned(std::min<int64_t>((nv + 255) / 256, 4096));
+    fixed_to_float_kernel<<<cb, 256, 0, st>>>(iq, scales, dq, nv);
+    fixed_to_float_kernel<<<cb, 256, 0, st>>>(ik, scales + 1, dk, nv);
+    const unsigned fb = unsigned(std::min<int64_t>((nfl + 255) / 256, 4096));
+    fixed_to_float_kernel<<<fb, 256, 0, st>>>(iff, scales + 2, dff, nfl);
+    fixed_to_float_kernel<<<fb, 256, 0, st>>>(ibf, scales + 2, dbf, nfl);
+    return 13;
 }
 
 }  // namespace snls_gpu

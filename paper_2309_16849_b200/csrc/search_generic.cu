@@ -286,6 +286,35 @@ __global__ void emit_tape_kernel(const float* ff, const float* bf, Dims d, int w
     }
 }
 
+// The reference's fp64 SearchTape (search.hpp:89-110) from the device tape: absolute key
+// centres (kt, ky, kx) and absolute chain links, recomputed in fp64 from the flows exactly
+// as emit_row builds them (search.cpp:207-234): ky = (qy + sdy) + stride1 * (dyi - ws/2), the
+// window index dyi recovered from the fp32 offset (its rounding is far below stride1 / 2).
+__global__ void tape64_kernel(const float* ff, const float* bf, Dims d, int ws, int wt, int topl,
+                              double stride1, const float* offsets, double* centers,
+                              double* chains) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= d.rows * topl) return;
+    const int64_t row = e / topl;
+    int qt, qy, qx;
+    row_coords(d, row, qt, qy, qx);
+    const float* o = offsets + size_t(e) * 3;
+    const int dt = int(rintf(o[0]));
+    const int cs = wt > 1 ? wt - 1 : 0;
+    double* lk = chains ? chains + size_t(e) * cs * 6 : nullptr;
+    if (lk)
+        for (int j = 0; j < cs * 6; ++j) lk[j] = 0.0;
+    double sdy = 0.0, sdx = 0.0;
+    const int kt = qt + dt;
+    if (kt >= 0 && kt < d.t) shift_to_t<double>(ff, bf, d.h, d.w, qt, qy, qx, dt, sdy, sdx,
+                                                (dt > 1 || dt < -1) ? lk : nullptr);
+    const double ny = rint((double(o[1]) - sdy) / stride1), nx = rint((double(o[2]) - sdx) / stride1);
+    double* c = centers + size_t(e) * 3;
+    c[0] = double(kt);
+    c[1] = (double(qy) + sdy) + stride1 * ny;
+    c[2] = (double(qx) + sdx) + stride1 * nx;
+}
+
 // replay_similarities (search.cpp:470-493): one thread per selected entry.
 template <int VEC>
 __global__ void replay_kernel(const float* q, const float* k, Dims d, int ps, int metric,
@@ -372,6 +401,14 @@ int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,
     const int64_t n = d.rows * topl;
     emit_tape_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(ff, bf, d, wt, topl, offsets,
                                                                chains);
+    return 1;
+}
+
+int launch_tape64(const float* ff, const float* bf, Dims d, int ws, int wt, int topl, double stride1,
+                  const float* offsets, double* centers, double* chains, cudaStream_t st) {
+    const int64_t n = d.rows * topl;
+    tape64_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(ff, bf, d, ws, wt, topl, stride1, offsets,
+                                                            centers, chains);
     return 1;
 }
 

@@ -143,6 +143,8 @@ def lib() -> C.CDLL:
             L.snls_align_frames.argtypes = [VOIDP, P, _Dims, VOIDP, C.c_double, C.c_uint64, C.c_int,
                                             VOIDP, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
+            L.snls_search_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 11 + [C.c_int]
+            L.snls_search_tape64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 5
             L.snls_wpsum_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7
             L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
             L.snls_host_unregister.argtypes = [VOIDP]
@@ -264,8 +266,12 @@ def _ptr(t):
         raise SnlsError("snls: tensors must live on a CUDA device")
     if not t.is_contiguous():
         raise SnlsError("snls: tensors must be contiguous")
-    if t.dtype not in (torch.float32, torch.int32):
+    if t.dtype not in (torch.float32, torch.int32, torch.float64):
         raise SnlsError(f"snls: unsupported dtype {t.dtype}")
+    if t.data_ptr() % 16:
+        # the kernels load float4 vectors from the base pointers: a misaligned view would
+        # fault (and a misaligned-address fault poisons the whole CUDA context)
+        raise SnlsError("snls: tensor storage must be 16-byte aligned (use .clone() on a view)")
     return VOIDP(t.data_ptr())
 
 
@@ -389,10 +395,36 @@ def replay_similarities(res: SearchResult, q, k, ctx=None):
     return sims
 
 
-def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=True, frames=None):
+def search_tape64(res: SearchResult, fflow, bflow, ctx=None, frames=None):
+    """The reference's fp64 SearchTape (search.hpp:89-110) of a device result: absolute
+    centres rows x L x 3 and (wt > 1) absolute chain links rows x L x (wt-1) x 6, float64."""
+    import torch
+
+    ctx = ctx or context(res.sims.device.index)
+    cfg = res.cfg
+    c = _cfg(cfg)
+    if fflow is None:
+        raise SnlsError("search_tape64: pass the flows (zeros for nls_forward)")
+    t, h, w = fflow.shape[:3]
+    t0, t1 = frames if frames is not None else (0, t)
+    rows, L = res.sims.shape
+    cen = torch.empty((rows, L, 3), device=res.sims.device, dtype=torch.float64)
+    ch = (torch.empty((rows, L, cfg.chain_stride(), 6), device=res.sims.device, dtype=torch.float64)
+          if cfg.wt > 1 else None)
+    _raise(lib().snls_search_tape64(ctx.h, C.byref(c), _Dims(t, h, w, 1), int(t0), int(t1),
+                                    _ptr(fflow), _ptr(bflow), _ptr(res.offsets), _ptr(cen), _ptr(ch)))
+    ctx.sync_check()
+    return cen, ch
+
+
+def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=True, frames=None,
+                         deterministic=False, tape64=None):
     """snls::shifted_nls_backward (search.hpp:151-153) -> (dq, dk, dfflow, dbflow).
     `frames=(t0, t1)`: the tape holds the rows of query frames [t0, t1) only (frame
-    sharding); the gradients still cover every frame of q / k."""
+    sharding); the gradients still cover every frame of q / k.  `deterministic`: the
+    reference's default mode (bitwise reproducible, search.cpp:687-696).  `tape64`:
+    (centers, chains64) -- the reference's fp64 tape (search_tape64) instead of the device
+    tape."""
     import torch
 
     ctx = ctx or context(q.device.index)
@@ -405,9 +437,12 @@ def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=Tru
     dk = torch.empty_like(q)
     dff = torch.empty((t, h, w, 2), device=q.device, dtype=torch.float32)
     dbf = torch.empty_like(dff)
-    _raise(lib().snls_search_bwd_frames(ctx.h, C.byref(c), _dims(q), int(t0), int(t1), _ptr(grad_sims),
-                                        _ptr(res.offsets), _ptr(res.chains), _ptr(q), _ptr(k),
-                                        _ptr(dq), _ptr(dk), _ptr(dff), _ptr(dbf)))
+    cen, ch64 = tape64 if tape64 is not None else (None, None)
+    _raise(lib().snls_search_bwd_ex(ctx.h, C.byref(c), _dims(q), int(t0), int(t1), _ptr(grad_sims),
+                                    None if cen is not None else _ptr(res.offsets),
+                                    None if cen is not None else _ptr(res.chains), _ptr(cen),
+                                    _ptr(ch64), _ptr(q), _ptr(k), _ptr(dq), _ptr(dk), _ptr(dff),
+                                    _ptr(dbf), 1 if deterministic else 0))
     if check:
         ctx.sync_check()
     return dq, dk, dff, dbf

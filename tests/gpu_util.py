@@ -67,28 +67,128 @@ def rel_chains(chains_abs, cfg: Cfg, t, h, w, offsets=None):
     return c
 
 
-def compare_search(res, sims_ref, offs_ref, cfg: Cfg, sims_lplus1=None, exact=False,
-                   exact_ties=False):
-    """Selected values within REL_TOL everywhere; offsets equal on rows whose oracle ranking
-    has no near-tie (exact ties must still resolve by scan order); with `exact` (integer
-    inputs) everything must match bit for bit.  Returns the number of excluded rows."""
+EPS32 = 2.0 ** -23  # fp32 machine epsilon
+
+
+def rms(a) -> float:
+    a = np.asarray(a, np.float64)
+    return float(np.sqrt(np.mean(a * a))) if a.size else 0.0
+
+
+def fp32_bound(sims, cfg: Cfg, q, k, mult: float = 8.0):
+    """Per-row bound on the fp32 error of one similarity: mult * eps32 * sum|terms|, with
+    sum|terms| estimated as |s| (l2: every term has the same sign) plus ps^2*C*rms(q)*rms(k)
+    (the inner-product magnitude and the bilinear-sample rounding).  Two candidates whose
+    fp64 values are closer than this may legitimately swap ranks in fp32."""
+    s = np.asarray(sims, np.float64)
+    n = cfg.ps * cfg.ps * np.asarray(q).shape[-1]
+    base = n * rms(q) * rms(k)
+    finite = np.where(np.isfinite(s), np.abs(s), 0.0)
+    return mult * EPS32 * (finite.max(axis=1) + base)
+
+
+def oracle_ranked(chk, q, k, ff, bf, cfg: Cfg):
+    """The oracle's top-(L+1) (its first L ranks are the top-L, search.cpp:187-197), or the
+    top-L when fewer than L+1 window entries are valid for some query."""
+    try:
+        return chk.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))
+    except Exception:
+        return chk.search_fwd(q, k, ff, bf, cfg)
+
+
+def _match(a, b):
+    return np.all(np.abs(a - b) <= 1e-6 * np.maximum(1.0, np.abs(b)))
+
+
+def compare_search(res, ref, cfg: Cfg, q=None, k=None, *, exact=False, exact_ties=False,
+                   max_skip=0.01, mult=8.0, label=""):
+    """Check the device's selection against the oracle's on EVERY row.
+
+    `ref` holds the oracle's ranked list (sims, offsets) with L or L+1 columns
+    (oracle_ranked).  Selected values must agree within REL_TOL at every rank.  Offsets must
+    be equal at every rank except inside a cluster of oracle ranks whose adjacent fp64 gaps
+    are below the fp32 error bound (fp32_bound): an interior cluster must hold the same
+    candidates (order within the cluster is free), and a cluster that reaches rank L+1 (a
+    near-tie across the top-L boundary) may exchange its members with the next ranks; such
+    rows are 'skipped', counted, printed and capped at `max_skip` of the rows (boundary
+    clusters of exactly equal fp64 values are counted as 'exact_ties' instead).  With
+    `exact_ties` an exact fp64 tie never forms a cluster, so it must resolve by scan order
+    exactly as in the reference (search.cpp:187-197).  With `exact` (integer-valued inputs:
+    every fp32 sum is exact) sims and offsets must be bitwise equal.  Returns the counts."""
     sims = host(res.sims)
     offs = host(res.offsets)
+    L = cfg.topl
+    s_all = np.asarray(ref["sims"], np.float64)
+    o_all = np.asarray(ref["offsets"], np.float64)
+    s_ref, o_ref = s_all[:, :L], o_all[:, :L]
+    rows = s_ref.shape[0]
+    stats = {"rows": rows, "mismatched": 0, "tie_order": 0, "skipped": 0, "exact_ties": 0}
     if exact:
-        assert np.array_equal(sims, sims_ref), "sims differ on integer-valued inputs"
-        assert np.array_equal(offs, offs_ref), "offsets differ on integer-valued inputs"
-        return 0
-    assert max_rel(sims, sims_ref) <= REL_TOL, max_rel(sims, sims_ref)
-    s = np.asarray(sims_lplus1 if sims_lplus1 is not None else sims_ref)
-    k = min(s.shape[1], cfg.topl + 1)
-    gaps = s[:, : k - 1] - s[:, 1:k]
-    scale = np.maximum(1.0, np.abs(s[:, : k - 1]))
-    # Exact fp64 ties are kept (must resolve by scan order) only when the tied candidates are
-    # the same computation (ps == 1 border reflection); with ps > 1 a reflected window can
-    # hold a permutation of the same terms, which ties in fp64 by luck but not in fp32.
-    lo = 0.0 if exact_ties else -1.0
-    near = np.any((gaps > lo) & (gaps < 1e-4 * scale), axis=1)
-    keep = ~near
-    d = np.abs(offs[keep] - offs_ref[keep]) / np.maximum(1.0, np.abs(offs_ref[keep]))
-    assert d.size == 0 or d.max() <= 1e-6, (d.max(), np.argwhere(d > 1e-6)[:5])
-    return int(near.sum())
+        assert np.array_equal(sims, s_ref), "sims differ on integer-valued inputs"
+        assert np.array_equal(offs, o_ref), "offsets differ on integer-valued inputs"
+        print(f"[compare_search{label}] {stats}")
+        return stats
+    assert max_rel(sims, s_ref) <= REL_TOL, max_rel(sims, s_ref)
+    same = np.all(np.abs(offs - o_ref) <= 1e-6 * np.maximum(1.0, np.abs(o_ref)), axis=(1, 2))
+    bad = np.flatnonzero(~same)
+    stats["mismatched"] = int(bad.size)
+    if q is not None and k is not None:
+        # observed fp32 error of the selected values in units of the bound's eps32*sum|terms|
+        unit = fp32_bound(s_ref, cfg, q, k, 1.0)
+        fin = np.isfinite(s_ref)
+        err = np.where(fin, np.abs(np.where(fin, sims, 0.0) - np.where(fin, s_ref, 0.0)), 0.0)
+        stats["err_units"] = round(float((err / unit[:, None]).max()), 3) if rows else 0.0
+    if bad.size:
+        assert q is not None and k is not None, "near-tie analysis needs q and k"
+        tol = fp32_bound(s_all[bad], cfg, q, k, mult)
+    have_next = s_all.shape[1] > L
+    failures = []
+    for i, r in enumerate(bad):
+        s, o = s_all[r], o_all[r]
+        gaps = s[:-1] - s[1:]
+        link = gaps < tol[i]
+        if exact_ties:
+            link &= gaps > 0
+        a, boundary, exact_tie, ok = 0, False, True, True
+        while a < L:
+            b = a
+            while b < len(link) and link[b]:
+                b += 1
+            got = offs[r, a:min(b, L - 1) + 1]
+            want = o[a:b + 1]
+            if have_next and b == len(s) - 1 and b > a:
+                # near-tie across the boundary: a device pick in the cluster's top-L part is
+                # one of its known members or an unlisted rank beyond L+1 tied with them --
+                # never a candidate the oracle ranks outside the cluster
+                boundary = True
+                # an fp64 tie (gaps at fp64 rounding level, <= 1e-12 |s|: e.g. a border
+                # window whose reflection holds a permutation of another's terms) is no fp32
+                # accuracy question -- counted apart from the near-ties
+                exact_tie = exact_tie and bool(np.all(gaps[a:b] <= 1e-12 * max(1.0, abs(s[a]))))
+                others = np.concatenate([o[:a], o[b + 1:]])
+                for g in got:
+                    if not any(_match(g, x) for x in want) and any(_match(g, x) for x in others):
+                        ok = False
+            else:
+                used = np.zeros(len(want), bool)
+                for g in got:
+                    hit = [j for j in range(len(want)) if not used[j] and _match(g, want[j])]
+                    if not hit:
+                        ok = False
+                        break
+                    used[hit[0]] = True
+            a = b + 1
+        if not ok:
+            failures.append(int(r))
+        elif boundary and exact_tie:
+            stats["exact_ties"] += 1
+        elif boundary:
+            stats["skipped"] += 1
+        else:
+            stats["tie_order"] += 1
+    print(f"[compare_search{label}] {stats}")
+    assert not failures, (f"{len(failures)} rows select different candidates outside any "
+                          f"fp32 near-tie, e.g. row {failures[0]}: device "
+                          f"{offs[failures[0]].tolist()} oracle {o_all[failures[0]].tolist()}")
+    assert stats["skipped"] <= max_skip * rows, stats
+    return stats

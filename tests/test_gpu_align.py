@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import Cfg, Checker, have_reference
-from tests.gpu_util import dev, host, snls_mod
+from tests.gpu_util import dev, fp32_bound, host, snls_mod
 from tests.helpers import REL_TOL, max_rel
 
 pytestmark = pytest.mark.gpu
@@ -66,17 +66,23 @@ def test_align_frames_vs_oracle_composition(source):
     noisy = S.add_gaussian_noise(clean.astype(np.float32), 10.0, 5).astype(np.float64)
     want = P.align_frames(clean, cfg, source=source, bm_block=5, bm_radius=3, noisy=noisy)
     assert np.array_equal(r["used_flow"], want["used_flow"])
-    # selection: equal except rows whose oracle top-2 gap is a (near-)tie -- incl. exact fp64
-    # ties of reflected permutations (gradcheck_util.hpp:61-69)
+    # selection: equal except rows whose oracle top-2 gap is within the fp32 error bound
+    # (tests/gpu_util.fp32_bound) -- incl. exact fp64 ties of reflected permutations
     nq = want["offsets"].shape[0] // (t - 1)
     zb = np.zeros((1, h, w, 2))
     c2 = Cfg(**{**cfg.__dict__, "topl": 2})
-    near = np.concatenate([
-        (lambda s2: (s2[:, 0] - s2[:, 1]) < 1e-4 * np.maximum(1, np.abs(s2[:, 0])))(
-            P.search_fwd(noisy[ti:ti + 1], noisy[ti + 1:ti + 2], want["used_flow"][ti:ti + 1], zb, c2)["sims"])
+    s2 = np.concatenate([
+        P.search_fwd(noisy[ti:ti + 1], noisy[ti + 1:ti + 2], want["used_flow"][ti:ti + 1], zb, c2)["sims"]
         for ti in range(t - 1)])
+    gap = s2[:, 0] - s2[:, 1]
+    near = gap <= fp32_bound(s2, cfg, noisy, noisy)
     same = np.all(r["top1_offsets"] == want["offsets"], axis=1)
     assert np.all(same | near), np.argwhere(~(same | near))[:5]
+    # fp64 ties (reflected permutations of the same terms, equal to fp64 rounding)
+    exact = ~same & (gap <= 1e-12 * np.maximum(1.0, np.abs(s2[:, 0])))
+    print(f"[align] rows {same.size}, differing: exact fp64 ties {int(exact.sum())}, "
+          f"fp32 near-ties {int((~same & ~exact).sum())}")
+    assert (~same & ~exact).sum() <= 0.01 * same.size
     # aggregation + PSNR of the device's own selection (top-1 weight is exactly 1)
     for ti in range(t - 1):
         o = r["top1_offsets"][ti * nq:(ti + 1) * nq].astype(np.float64).reshape(nq, 1, 3)

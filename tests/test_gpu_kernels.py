@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import Cfg
-from tests.gpu_util import compare_search, dev, host, scfg, snls_mod
+from tests.gpu_util import compare_search, dev, host, oracle_ranked, scfg, snls_mod
 from tests.helpers import REL_TOL, flow, max_rel, video
 
 pytestmark = pytest.mark.gpu
@@ -31,10 +31,9 @@ def case(port, name, t, h, w, f, cfg):
         q = video(port, t, h, w, f, seed)
         k = q if name != "c2" else video(port, t, h, w, f, seed + 1)
         ff, bf = flow(port, t, h, w, seed + 3, 2.0), flow(port, t, h, w, seed + 4, 2.0)
-        ref = port.search_fwd(q, k, ff, bf, cfg)
-        lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
-        wts = port.softmax_rows(ref["sims"], cfg.softmax_scale)
-        _cache[name] = (q, k, ff, bf, ref, lp1, wts)
+        ref = oracle_ranked(port, q, k, ff, bf, cfg)
+        wts = port.softmax_rows(ref["sims"][:, :cfg.topl], cfg.softmax_scale)
+        _cache[name] = (q, k, ff, bf, ref, wts)
     return _cache[name]
 
 
@@ -42,16 +41,14 @@ def case(port, name, t, h, w, f, cfg):
 @pytest.mark.parametrize("name,t,h,w,f,cfg", SHAPES, ids=[s[0] for s in SHAPES])
 def test_register_plan_vs_oracle(port, kernel, path, name, t, h, w, f, cfg):
     S = snls_mod()
-    q, k, ff, bf, ref, lp1, wts = case(port, name, t, h, w, f, cfg)
+    q, k, ff, bf, ref, wts = case(port, name, t, h, w, f, cfg)
     ctx = S.context()
     ctx.set_search_kernel(kernel)
     try:
         args = (dev(q), dev(k), dev(ff), dev(bf), scfg(cfg))
         r = S.shifted_nls_forward(*args, want_weights=True, ctx=ctx)
         assert ctx.last_search_path() == path
-        excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
-        # near-tie rows (gradcheck_util.hpp:61-69) are common with k = 16 of 847 candidates
-        assert excluded < 0.5 * ref["sims"].shape[0]
+        compare_search(r, ref, cfg, q, k, label=f" {name} {kernel}")
         assert max_rel(host(r.weights), wts) <= REL_TOL
         g = S.shifted_nls_forward(*args, mode=1, want_weights=True, ctx=ctx)
         for x, y in ((r.sims, g.sims), (r.offsets, g.offsets), (r.weights, g.weights)):
@@ -68,7 +65,7 @@ def test_wpsum_at_baseline_shapes_stage_isolated(port, name, t, h, w, f, cfg):
     """wpsum / gather_stack at the BASELINE F / ps / stride0 (c5: F = 64 runs the query-centric
     kernel as two channel slices) against the oracle on the device's own selection."""
     S = snls_mod()
-    q, k, ff, bf, ref, lp1, wts = case(port, name, t, h, w, f, cfg)
+    q, k, ff, bf, ref, wts = case(port, name, t, h, w, f, cfg)
     v = video(port, t, h, w, f, 777)
     r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), want_weights=True)
     out, cnt = S.wpsum(dev(v), r.weights, r.offsets, scfg(cfg))
@@ -97,8 +94,7 @@ def test_tiled_plan_matrix_vs_oracle(port, ps, ws, f, metric):
     seed = 7000 + 97 * ps + 13 * ws + f + (1 if metric == "l2" else 0)
     q, k = video(port, t, h, w, f, seed), video(port, t, h, w, f, seed + 1)
     ff, bf = flow(port, t, h, w, seed + 2, 2.0), flow(port, t, h, w, seed + 3, 2.0)
-    ref = port.search_fwd(q, k, ff, bf, cfg)
-    lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
+    ref = oracle_ranked(port, q, k, ff, bf, cfg)
     ctx = S.context()
     ctx.set_search_kernel("tiled")
     try:
@@ -106,9 +102,7 @@ def test_tiled_plan_matrix_vs_oracle(port, ps, ws, f, metric):
         assert ctx.last_search_path() == 1, "expected the tiled kernel for this shape"
     finally:
         ctx.set_search_kernel("auto")
-    excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
-    # large-|s| L2 rows (ps 7, F 64: |s| ~ 2e3) are often within 1e-4 |s| of a neighbour rank
-    assert excluded < 0.75 * ref["sims"].shape[0]
+    compare_search(r, ref, cfg, q, k, label=f" p{ps}w{ws}f{f}{metric}")
 
 
 def test_c2_stride1_search_row(port):
@@ -118,13 +112,11 @@ def test_c2_stride1_search_row(port):
     t, h, w, f = 5, 12, 14, 64
     q, k = video(port, t, h, w, f, 11), video(port, t, h, w, f, 12)
     ff, bf = flow(port, t, h, w, 14, 2.0), flow(port, t, h, w, 15, 2.0)
-    ref = port.search_fwd(q, k, ff, bf, cfg)
-    lp1 = port.search_fwd(q, k, ff, bf, Cfg(**{**cfg.__dict__, "topl": cfg.topl + 1}))["sims"]
+    ref = oracle_ranked(port, q, k, ff, bf, cfg)
     ctx = S.context()
     r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), ctx=ctx)
     assert ctx.last_search_path() == 1
-    excluded = compare_search(r, ref["sims"], ref["offsets"], cfg, lp1)
-    assert excluded < 0.5 * ref["sims"].shape[0]
+    compare_search(r, ref, cfg, q, k, label=" c2 stride0=1")
 
 
 EXACT = [(11, 3, 32, "l2", 16), (11, 3, 32, "l2", 17), (11, 3, 32, "l2", 40), (11, 3, 32, "l2", 100),
@@ -151,4 +143,4 @@ def test_topl_sizes_bit_exact_on_integer_inputs(port, ws, ps, f, metric, topl):
         r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), ctx=ctx, mode=mode)
         if mode == 0:
             assert ctx.last_search_path() == (1 if topl <= 16 else 0)
-        compare_search(r, ref["sims"], ref["offsets"], cfg, exact=True)
+        compare_search(r, ref, cfg, exact=True)

@@ -2,8 +2,15 @@
 """Benchmark: Shifted Non-Local Search forward (search + top-L + softmax + wpsum aggregate) on
 B200, the BASELINE.json metric "search+aggregate queries/sec (ms/video) & %roofline".
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2|c3|c5]
+                    [--videos-per-gpu V] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+
+`--gpus N` without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks (127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal N.
+`--videos-per-gpu V` (c4): each rank processes V independent videos per step, so SURVEY 8e's
+scaling ratio t(8 videos on 1 GPU) / t(1 video per GPU on 8) is `--gpus 1 --videos-per-gpu 8`
+against `--gpus 8`.
 
 Workload (default c4 = BASELINE configs[3]): one 10x256x256x32 video per GPU, ws 11, wt 3,
 ps 3, k 16, L2, stride0 2, beta 1/288, fractional flows U[-2,2); Q = K = V as in the
@@ -192,6 +199,27 @@ def make_inputs(S, wl, b):
     return vid, ff.reshape(T, H, W, 2), bf.reshape(T, H, W, 2)
 
 
+def init_dist(world, local, backend):
+    """One process per GPU; NCCL's INIT lines (communicator size) go to stderr as evidence of
+    the N-rank communicator.  Returns the communicator description for the JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    if world <= 1:
+        return None
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()  # eager communicator creation (device_id) + one collective
+    else:
+        dist.init_process_group("gloo")
+    n = dist.get_world_size()
+    assert n == world, f"communicator has {n} ranks, WORLD_SIZE says {world}"
+    print(f"[bench] rank {dist.get_rank()}: {backend} communicator nranks={n}", file=sys.stderr, flush=True)
+    return {"backend": backend, "nranks": n}
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
@@ -200,11 +228,13 @@ def run_ours(args, wl):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = init_dist(world, local, "nccl")
     dev = torch.device("cuda", local)
     model = work_model(wl)
     rows = model["rows"]
+    nvid = max(1, args.videos_per_gpu)
+    if nvid > 1 and (wl.get("sharded") or wl.get("train")):
+        raise SystemExit("--videos-per-gpu applies to the batch workloads (c4, c2)")
     cfg = S.SearchConfig(ws=wl["ws"], wt=wl["wt"], ps=wl["ps"], stride0=wl["stride0"],
                          stride1=1.0, topl=wl["topl"], metric=wl["metric"], softmax_scale=wl["beta"])
     sharded = wl.get("sharded", False)
@@ -216,12 +246,21 @@ def run_ours(args, wl):
         frames = (plan.t0, plan.t1)
         rows = (plan.b - plan.a) * (rows // wl["T"])
     else:
-        vid_h, ff_h, bf_h = make_inputs(S, wl, rank)
+        # video b = rank * V + j (seeds 100+b / 200+b / 300+b)
+        vid_h, ff_h, bf_h = make_inputs(S, wl, rank * nvid)
         frames = None
     own_vid = torch.from_numpy(vid_h).to(dev)
     own_ff = torch.from_numpy(ff_h).to(dev)
     own_bf = torch.from_numpy(bf_h).to(dev)
     vid, ff, bf = own_vid, own_ff, own_bf
+    # the other videos of this rank (independent inputs, own output buffers)
+    extra = []
+    for j in range(1, nvid):
+        vh, fh, bh = make_inputs(S, wl, rank * nvid + j)
+        extra.append(tuple(torch.from_numpy(x).to(dev) for x in (vh, fh, bh)) +
+                     (torch.empty((rows, wl["topl"]), device=dev), torch.empty((rows, wl["topl"], 3), device=dev),
+                      torch.empty((rows, wl["topl"]), device=dev), torch.empty_like(own_vid),
+                      torch.empty(own_vid.shape[:3], device=dev, dtype=torch.int32)))
     if sharded:  # persistent slabs [lo, hi): owned frames in place, halo frames refilled by
         # the in-place NCCL exchange every step (overlapped with the interior frames)
         def slab_of(own):
@@ -256,8 +295,12 @@ def run_ours(args, wl):
             return
         res = S.shifted_nls_forward(vid, vid, ff, bf, cfg, ctx=ctx, check=False,
                                     out=(sims, offs, chains if train else None, wts), frames=frames)
+        for (xv, xf, xb, xs, xo, xw, _, _) in extra:  # further videos of this rank: search
+            S.shifted_nls_forward(xv, xv, xf, xb, cfg, ctx=ctx, check=False, out=(xs, xo, None, xw))
         ev_mid.record(stream)
         S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
+        for (xv, _, _, _, xo, xw, xout, xcnt) in extra:  # ... and aggregation
+            S.wpsum(xv, xw, xo, cfg, ctx=ctx, check=False, out=(xout, xcnt))
         if train:  # backward: wpsum_backward (dV, dW) then shifted_nls_backward (dQ, dK, dFlow)
             ev_bwd.record(stream)
             S.wpsum_backward(g_out, counts, vid, wts, offs, cfg, ctx=ctx, check=False)
@@ -356,6 +399,8 @@ def run_ours(args, wl):
             offs_p.copy_(offs, non_blocking=True)
             out_p.copy_(out, non_blocking=True)
 
+    # further videos of the rank go through the same call one after another: they copy the
+    # same bytes as video 0, so e2e per step = V clips (timed per clip below, x V)
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
@@ -400,6 +445,9 @@ def run_ours(args, wl):
         e2e_wall_ms = (time.perf_counter() - w0) * 1e3 / n_e2e
         e2e_ms = a.elapsed_time(b) / n_e2e
         assert torch.equal(outs[1][2], out_p) and torch.equal(outs[1][0], sims_p)
+    e2e_ms *= nvid
+    e2e_sync_ms *= nvid
+    e2e_wall_ms *= nvid
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -409,22 +457,22 @@ def run_ours(args, wl):
         # the pipeline's results are the device path's results (same kernels, same rows)
         assert torch.equal(sims_p, sims.cpu()) and torch.equal(out_p, out.cpu()), \
             "host-buffer pipeline disagrees with the device-resident step"
-    h2d = vid_h.nbytes + ff_h.nbytes + bf_h.nbytes
-    d2h = sims_p.numel() * 4 + offs_p.numel() * 4 + out_p.numel() * 4
+    h2d = (vid_h.nbytes + ff_h.nbytes + bf_h.nbytes) * nvid
+    d2h = (sims_p.numel() * 4 + offs_p.numel() * 4 + out_p.numel() * 4) * nvid
 
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
-    total_rows = model["rows"] if sharded else rows * world
+    total_rows = model["rows"] if sharded else rows * world * nvid
     P, peak_src = peaks()
     sm_max = float(P.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak_tflops = nsm * 128 * 2 * sm_max * 1e6 / 1e12
     t_search = tot_search / args.steps / 1e3
     share = rows / model["rows"]  # this rank's fraction of the video (frame sharding)
-    achieved = 2.0 * model["search_instr"] * share / t_search / 1e12
+    achieved = 2.0 * model["search_instr"] * share * nvid / t_search / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -440,18 +488,20 @@ def run_ours(args, wl):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
-        "ms_per_video": ms_per_step,
+        "ms_per_video": ms_per_step / nvid,
         "higher_is_better": True,
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic: reference UniformStream video U[-1,1) (Q=K=V) and flows U[-2,2)",
         "config": {"workload": wl["name"],
-                   "videos_per_gpu": 1 if not sharded else f"1/{world} (frames {plan.a}..{plan.b - 1} on rank 0)",
-                   "queries_per_gpu": rows,
+                   "videos_per_gpu": nvid if not sharded else f"1/{world} (frames {plan.a}..{plan.b - 1} on rank 0)",
+                   "global_batch": nvid * world if not sharded else 1,
+                   "queries_per_gpu": rows * nvid,
                    "parallelism": (f"frame-sharded x{world}, wt-frame halo via NCCL send/recv"
                                    if sharded else f"batch-sharded x{world} (no collective)"),
                    "l2": "flushed (512 MB memset) between timed steps"},
+        "comm": comm,
         "breakdown_ms": {("search_topl_softmax" if not overlapped else
                           "search_softmax_wpsum_with_halo_exchange"): tot_search / args.steps,
                          "wpsum": statistics.mean(wpsum_ms),
@@ -461,7 +511,7 @@ def run_ours(args, wl):
                      "frac": achieved / fp32_peak_tflops, "traffic": traffic,
                      "algorithmic": f"{model['search_instr']:.4g} FMA-pipe instr/video x2 flop",
                      "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x sm_max_mhz from {peak_src}",
-                     "hbm_frac": model["bytes_search"] * share / t_search / 1e9 / float(P.get("hbm_gbs", 6650))},
+                     "hbm_frac": model["bytes_search"] * share * nvid / t_search / 1e9 / float(P.get("hbm_gbs", 6650))},
         "e2e": {"value": total_rows / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "wall_ms_per_step": e2e_wall_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -469,7 +519,9 @@ def run_ours(args, wl):
                 "api": ("snls_pipeline_submit/wait (C-ABI, a stream of clips from pinned host "
                         f"buffers, {chunk} frame(s)/chunk, three clips in flight; "
                         "sync_ms_per_step = one clip at a time, snls_pipeline_run, 1 frame/chunk)") if use_pipe else
-                       "torch H2D + NCCL halo + snls_search_fwd_frames/wpsum_fwd_frames + D2H"},
+                       ("torch H2D + NCCL halo + snls_search_fwd_frames/wpsum_fwd_frames + D2H" if overlapped else
+                        "torch H2D + snls_search_fwd / snls_wpsum_fwd" +
+                        (" / snls_wpsum_bwd / snls_search_bwd_ex" if train else "") + " (C-ABI) + D2H")},
         "gpu_launches": launches,
         "clocks": clk,
         "wall_s_timed_loop": wall,
@@ -523,6 +575,17 @@ def reference_sample(wl, crop):
     return R, rows, run
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(wl, budget_s=20.0):
     crop = 96
     R, rows, run = reference_sample(wl, crop)
@@ -535,7 +598,7 @@ def cpu_baseline(wl, budget_s=20.0):
             break
     med = statistics.median(times)
     return {"value": rows / med, "unit": UNIT, "cores": R.lib.ref_max_threads(),
-            "kind": "reference",
+            "kind": "reference", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
             "sample": (f"reference snls::shifted_nls_forward + softmax_rows + wpsum"
                        f"{' + wpsum_backward + shifted_nls_backward' if wl.get('train') else ''} (oracle/_ref, "
                        f"fp64, OpenMP all host threads) on a {wl['T']}x{crop}x{crop}x{wl['C']} crop "
@@ -562,7 +625,7 @@ def run_reference(args, wl):
         "config": {"workload": wl["name"], "sample": f"{wl['T']}x{crop}x{crop}x{wl['C']} crop",
                    "queries_per_step": rows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": R.lib.ref_max_threads(),
-                         "kind": "reference",
+                         "kind": "reference", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{wl['T']}x{crop}x{crop}x{wl['C']} crop, {rows} queries/step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -582,13 +645,78 @@ def main():
                     help="query frames per chunk of the e2e host pipeline (0: 1)")
     ap.add_argument("--search-kernel", default=os.environ.get("SNLS_SEARCH_KERNEL", "auto"),
                     choices=["auto", "tiled", "stream"], help="stride1 == 1 register plan")
+    ap.add_argument("--videos-per-gpu", type=int, default=1,
+                    help="independent videos per rank and step (c4/c2; SURVEY 8e scaling ratio)")
+    ap.add_argument("--mock-cpu", action="store_true",
+                    help="plumbing check without a GPU: gloo ranks, a numpy stand-in step, same "
+                         "launch / barrier / max-over-ranks / JSON path (tests/test_bench.py)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.mock_cpu:
+        run_mock(args, wl)
+    elif args.impl == "reference":
         run_reference(args, wl)
     else:
         run_ours(args, wl)
+
+
+def self_launch(n):
+    """`--gpus N` outside torchrun: re-run this command as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line reaches our stdout."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_mock(args, wl):
+    """The multi-rank harness without a GPU: gloo communicator, W warm-up and K timed steps of
+    a fixed numpy stand-in, barrier on both sides, max over ranks, one JSON line on rank 0.
+    Not a measurement (no kernels run) -- it exercises the launch path the driver uses."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    comm = init_dist(world, local, "gloo")
+    a = np.random.default_rng(rank).standard_normal((256, 256))
+
+    def step():
+        return float((a @ a).sum())
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    tot = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([tot], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t[0])
+    rows = work_model(wl)["rows"] * max(1, args.videos_per_gpu)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": rows * world / (tot / args.steps / 1e3),
+                          "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": tot / args.steps, "mock": True, "comm": comm,
+                          "config": {"workload": wl["name"], "videos_per_gpu": args.videos_per_gpu}}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -206,8 +206,8 @@ __device__ void build_descs(const AggArgs& a, int ti, const TileGeom& g, SampleD
         d.kbase = uint32_t(kt) * uint32_t(a.d.h) * uint32_t(a.d.w);
         const float oy = __ldg(o + 1), ox = __ldg(o + 2);
         const float fly = floorf(oy), flx = floorf(ox);
-        d.oy = fold_base(fly, a.d.h);
-        d.ox = fold_base(flx, a.d.w);
+        d.oy = int_base(fly);
+        d.ox = int_base(flx);
         d.doff = d.oy * a.d.w + d.ox;
         const float fy = oy - fly, fx = ox - flx;
         const float wv = __ldg(a.weights + e);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
             const float w00 = wv * ((1.f - fy) * (1.f - fx)), w01 = wv * ((1.f - fy) * fx);
             const float w10 = wv * (fy * (1.f - fx)), w11 = wv * (fy * fx);
             // sample (i, j) sits between raw rows by+i, by+i+1 and cols bx+j, bx+j+1
-            const int by = qy - HP + fold_base(fly, H), bx = qx - HP + fold_base(flx, W);
+            const int by = qy - HP + int_base(fly), bx = qx - HP + int_base(flx);
             const float4* vf = vbase + size_t(kt) * H * row4;
             float4 blk[P + 1][P + 1];
             if (by >= 0 && by + P < H && bx >= 0 && bx + P < W) {
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
         const float wv = __ldg(a.weights + e);
-        const int by = qy - HP + fold_base(fly, H), bx = qx - HP + fold_base(flx, W);
+        const int by = qy - HP + int_base(fly), bx = qx - HP + int_base(flx);
         unsigned bcol[P + 1];
 #pragma unroll
         for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);

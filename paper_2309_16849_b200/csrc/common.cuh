@@ -124,27 +124,28 @@ __device__ __forceinline__ Taps taps_from(int by, float fy, int bx, float fx, in
     return t;
 }
 
-// An integral coordinate (or displacement) as int.  Beyond +-2^30 only its class modulo the
-// reflection period 2(n-1) matters (tensor.cpp:23-29), so fold it there -- exactly, fb is
-// integral -- before the conversion: a huge finite flow (Middlebury marks unknown flow with
-// ~1e9-1e10) can then neither saturate the int nor overflow base + offset sums into an
-// out-of-bounds address.  inf/NaN fold to NaN and convert to 0 (already latched as errors).
-__device__ __forceinline__ int fold_base(double fb, int n) {
-    if (!(fabs(fb) < 1073741824.0)) fb = fmod(fb, n > 1 ? 2.0 * (n - 1) : 1.0);
-    return int(fb);
+// An integral coordinate (or displacement) as int, clamped to +-(2^31 - 2^24) first: exact
+// for every position the reference's own int conversion defines (up to ~2.13e9 px), while a
+// huge or non-finite flow (Middlebury marks unknown flow with ~1e9-1e10; the reference's
+// conversion is undefined there) can no longer saturate the int and overflow base + offset
+// sums into an out-of-bounds address.  NaN converts to 0 (flows are latched as errors).
+__device__ __forceinline__ int int_base(double fb) {
+    constexpr int kLim = 2147483647 - 16777216;
+    const int i = int(fb);  // cvt.rzi.s32.f64 saturates (and maps NaN to 0)
+    return min(max(i, -kLim), kLim);
 }
 
 // Position given in fp64 (absolute coordinate).
 __device__ __forceinline__ Taps taps_at(double y, double x, int h, int w) {
     const double by = floor(y), bx = floor(x);
-    return taps_from(fold_base(by, h), float(y - by), fold_base(bx, w), float(x - bx), h, w);
+    return taps_from(int_base(by), float(y - by), int_base(bx), float(x - bx), h, w);
 }
 
 // Position = integer `base` + fp32 `off` (off may be any magnitude that fp32 holds) along an
 // axis of n pixels.
 __device__ __forceinline__ void split_pos(int base, float off, int& ib, float& fr, int n) {
     const float fl = floorf(off);
-    ib = base + fold_base(double(fl), n);
+    ib = base + int_base(double(fl));
     fr = off - fl;  // exact (Sterbenz) for |off| >= 1 and for 0 <= off < 1
 }
 
@@ -193,7 +194,7 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
             const double py = double(qy) + sy, px = double(qx) + sx;
             const double fby = floor(py), fbx = floor(px);
             const double fy = py - fby, fx = px - fbx;
-            const int iby = fold_base(fby, h), ibx = fold_base(fbx, w);
+            const int iby = int_base(fby), ibx = int_base(fbx);
             const int y0 = reflect_near(iby, h), y1 = reflect_near(iby + 1, h);
             const int x0 = reflect_near(ibx, w), x1 = reflect_near(ibx + 1, w);
             const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);

@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
         const double* cp = centers + size_t(e) * 3;
         kt = int(cp[0]);
         const double fly = floor(cp[1]), flx = floor(cp[2]);
-        cby = fold_base(fly, d.h);
-        cbx = fold_base(flx, d.w);
+        cby = int_base(fly);
+        cbx = int_base(flx);
         cfy = cp[1] - fly;
         cfx = cp[2] - flx;
     } else {
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
             fx = float(cx - flx);
             ddy = (cy - fly) - double(fy);
             ddx = (cx - flx) - double(fx);
-            by = fold_base(fly, d.h) - HP;
-            bx = fold_base(flx, d.w) - HP;
+            by = int_base(fly) - HP;
+            bx = int_base(flx) - HP;
         } else {
             const float* o = offsets + size_t(e) * 3;
             kt = qt + int(rintf(__ldg(o)));
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
             const float fly = floorf(oy), flx = floorf(ox);
             fy = oy - fly;
             fx = ox - flx;
-            by = qy - HP + fold_base(fly, d.h);
-            bx = qx - HP + fold_base(flx, d.w);
+            by = qy - HP + int_base(fly);
+            bx = qx - HP + int_base(flx);
         }
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
         const float fy = float(cy - fby), fx = float(cx - fbx);
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
-        const int by = fold_base(fby, H) - HW - HP, bx = fold_base(fbx, Wd) - HW - HP;
+        const int by = int(fby) - HW - HP, bx = int(fbx) - HW - HP;  // (see search_tiled.cu)
         const float* kb = a.k + size_t(on ? kt : qt) * frame_elems + c0;
         // reflected column offsets of the region (tensor.cpp:23-29), once per frame
         unsigned xo[R + 1];

@@ -214,12 +214,14 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         const float fy = float(cy - fby), fx = float(cx - fbx);
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
-        const int by = fold_base(fby, H) - HW - HP, bx = fold_base(fbx, Wd) - HW - HP;
+        // (cvt saturates a huge shift; the int sums below may then wrap, which reflect_near maps
+        // back into the frame like any other index, and the interior test cannot overflow)
+        const int by = int(fby) - HW - HP, bx = int(fbx) - HW - HP;
         // VEC-granular addressing: per region row one 64-bit row base, per column a 32-bit
         // vector index (one IMAD.WIDE per load instead of 64-bit pointer math)
         const float* kframe = a.k + size_t(on ? kt : qt) * frame_elems + c0;
         const unsigned rowv = unsigned(Wd) * G;  // VEC-vectors per image row
-        const bool interior = __all_sync(0xffffffffu, bx >= 0 && bx + R < Wd);
+        const bool interior = __all_sync(0xffffffffu, bx >= 0 && bx < Wd - R);
         const unsigned xb = unsigned(bx) * G;
         // reflected column offsets, precomputed (recomputing them at the boundary-warp loads
         // instead: c4 5.06 vs 4.45 ms) and parked in shared memory: only boundary warps read

@@ -143,8 +143,9 @@ def lib() -> C.CDLL:
             L.snls_align_frames.argtypes = [VOIDP, P, _Dims, VOIDP, C.c_double, C.c_uint64, C.c_int,
                                             VOIDP, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
-            L.snls_search_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 11 + [C.c_int]
-            L.snls_search_tape64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 5
+            if hasattr(L, "snls_search_bwd_ex"):  # (absent from A/B builds of older trees)
+                L.snls_search_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 11 + [C.c_int]
+                L.snls_search_tape64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 5
             L.snls_wpsum_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7
             L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
             L.snls_host_unregister.argtypes = [VOIDP]

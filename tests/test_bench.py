@@ -41,3 +41,27 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_gpus_flag_self_launches_n_ranks(n):
+    """`python bench.py --gpus N` (no torchrun environment) re-launches itself as N ranks and
+    rank 0 reports n_gpus == N with an N-rank communicator (gloo stand-in step on CPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--mock-cpu", "--steps", "3",
+                        "--warmup", "3", "--videos-per-gpu", "2"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == n and line["comm"]["nranks"] == n
+    assert line["config"]["videos_per_gpu"] == 2
+    assert p.stderr.count("communicator nranks=") == n
+
+
+def test_world_size_mismatch_is_refused():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--mock-cpu"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode != 0 and "WORLD_SIZE" in (p.stderr + p.stdout)

@@ -228,7 +228,7 @@ def run_ours(args, wl):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    comm = init_dist(world, local, "nccl")
+    comm_info = init_dist(world, local, "nccl")
     dev = torch.device("cuda", local)
     model = work_model(wl)
     rows = model["rows"]
@@ -271,6 +271,14 @@ def run_ours(args, wl):
     overlapped = sharded and world > 1
     stream = torch.cuda.current_stream(dev)
     ctx = S.context(local)
+    # the halo moves over the C-ABI's own NCCL communicator (snls_halo_exchange_async); the
+    # torch.distributed group above is control plane only (id broadcast, barriers, max)
+    comm = SH.Comm.create(rank, world, ctx) if overlapped else None
+    if comm is not None:
+        ci = comm.info()
+        comm_info["snls_halo_comm"] = ci
+        print(f"[bench] rank {rank}: snls NCCL communicator nranks={ci['nranks']} "
+              f"(NCCL {ci['nccl_version']})", file=sys.stderr, flush=True)
     ctx.set_search_kernel(args.search_kernel)
     L = wl["topl"]
     sims = torch.empty((rows, L), device=dev)
@@ -289,7 +297,7 @@ def run_ours(args, wl):
 
     def step():
         if overlapped:  # the data path's only communication: the wt-frame halo (NCCL P2P)
-            SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, world=world,
+            SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, comm=comm,
                                            out=(sims, offs, None, wts, out, counts))
             ev_mid.record(stream)
             return
@@ -383,7 +391,7 @@ def run_ours(args, wl):
                 vid[plan.t0:plan.t1].copy_(vd)
                 ff[plan.t0:plan.t1].copy_(ffd)
                 bf[plan.t0:plan.t1].copy_(bfd)
-                SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, world=world,
+                SH.search_aggregate_overlapped(vid, vid, vid, ff, bf, plan, cfg, ctx=ctx, comm=comm,
                                                out=(sims, offs, None, wts, out, counts))
                 sims_p.copy_(sims, non_blocking=True)
                 offs_p.copy_(offs, non_blocking=True)
@@ -498,10 +506,10 @@ def run_ours(args, wl):
                    "videos_per_gpu": nvid if not sharded else f"1/{world} (frames {plan.a}..{plan.b - 1} on rank 0)",
                    "global_batch": nvid * world if not sharded else 1,
                    "queries_per_gpu": rows * nvid,
-                   "parallelism": (f"frame-sharded x{world}, wt-frame halo via NCCL send/recv"
+                   "parallelism": (f"frame-sharded x{world}, wt-frame halo via the C-ABI's NCCL send/recv"
                                    if sharded else f"batch-sharded x{world} (no collective)"),
                    "l2": "flushed (512 MB memset) between timed steps"},
-        "comm": comm,
+        "comm": comm_info,
         "breakdown_ms": {("search_topl_softmax" if not overlapped else
                           "search_softmax_wpsum_with_halo_exchange"): tot_search / args.steps,
                          "wpsum": statistics.mean(wpsum_ms),
@@ -519,7 +527,8 @@ def run_ours(args, wl):
                 "api": ("snls_pipeline_submit/wait (C-ABI, a stream of clips from pinned host "
                         f"buffers, {chunk} frame(s)/chunk, three clips in flight; "
                         "sync_ms_per_step = one clip at a time, snls_pipeline_run, 1 frame/chunk)") if use_pipe else
-                       ("torch H2D + NCCL halo + snls_search_fwd_frames/wpsum_fwd_frames + D2H" if overlapped else
+                       ("torch H2D + snls_halo_exchange_async (C-ABI NCCL) + snls_search_fwd_frames/"
+                        "wpsum_fwd_frames + D2H" if overlapped else
                         "torch H2D + snls_search_fwd / snls_wpsum_fwd" +
                         (" / snls_wpsum_bwd / snls_search_bwd_ex" if train else "") + " (C-ABI) + D2H")},
         "gpu_launches": launches,

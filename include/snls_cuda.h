@@ -181,6 +181,41 @@ int snls_search_tape64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, in
                        const float* fflow, const float* bflow, const float* offsets,
                        double* centers, double* chains64);
 
+/* ---- frame sharding across GPUs: shard plan + NCCL halos -------
+ * One video of T frames over `world` ranks: rank r owns query frames [a, b) (balanced
+ * contiguous split) and holds the slab [lo, hi) = [a-wt, b+wt) n [0, T) of K / V / flows; the
+ * wt-frame halo moves between owners by NCCL point-to-point send/recv (search.cpp:84-101,
+ * 300; wpsum writes only the query's own frame, aggregate.cpp:197-198).  Host-only plan:
+ * out4 = {a, b, lo, hi}; transfers: per message the peer, frames [lo, hi) and recv (1: from
+ * the peer into my slab, 0: my frames to the peer), peers ascending, recv before send. */
+int snls_shard_plan(int T, int world, int rank, int wt, int* out4);
+int snls_shard_transfers(int T, int world, int rank, int wt, int capacity, int* peer, int* lo,
+                         int* hi, int* recv, int* count);
+typedef struct snls_comm snls_comm;
+/* NCCL is loaded at first use (libnccl.so.2 already in the process, else the system one).
+ * Rank 0 makes the 128-byte id, the caller distributes it (any out-of-band channel), every
+ * rank calls snls_comm_init with its context (device) -- collective over the ranks. */
+int snls_comm_unique_id(void* id_out);
+int snls_comm_init(snls_ctx* ctx, const void* unique_id, int rank, int world, snls_comm** out);
+int snls_comm_destroy(snls_comm* comm);
+int snls_comm_info(snls_comm* comm, int* nranks, int* nccl_version);
+/* Forward halo: fill the halo frames of `nslabs` persistent frame-major DEVICE slabs [lo, hi)
+ * (owned frames in place; frame_bytes per slab; pass aliased slabs once) with one grouped
+ * ncclSend/ncclRecv set on the communicator's stream, ordered after the context's stream.
+ * Returns at once: enqueue the interior frames (no halo needed), then snls_halo_wait orders
+ * the context's stream after the transfer (no host block). */
+int snls_halo_exchange_async(snls_comm* comm, int T, int wt, int nslabs, void* const* slabs,
+                             const int64_t* frame_bytes);
+int snls_halo_wait(snls_comm* comm);
+/* Backward halo: partial gradients in my halo frames go to their owners; the partial sums
+ * the peers hold for my owned frames are received and added in place (fp32 slabs,
+ * frame_elems floats per frame).  Joined into the context's stream on return. */
+int snls_reverse_halo_add(snls_comm* comm, int T, int wt, int nslabs, float* const* slabs,
+                          const int64_t* frame_elems);
+/* NCCL self-check on one device: grouped send/recv of `bytes` from src to dst with this rank
+ * as its own peer, joined into the context's stream. */
+int snls_comm_loopback(snls_comm* comm, const void* src, void* dst, uint64_t bytes);
+
 /* ---- aggregate (aggregate.hpp) ------------------------------------------------------ */
 /* Replaces snls::softmax_rows (aggregate.hpp:22; aggregate.cpp:16-37). */
 int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims,

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsnls_cuda.so")
-SOURCES = ["capi.cu", "search_generic.cu", "search_tiled.cu", "search_stream.cu", "search_bwd.cu", "aggregate.cu", "pipeline.cu", "align.cu", "io.cu"]
+SOURCES = ["capi.cu", "search_generic.cu", "search_tiled.cu", "search_stream.cu", "search_bwd.cu", "aggregate.cu", "pipeline.cu", "align.cu", "io.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -49,7 +49,7 @@ def build(verbose: bool = False, force: bool = False, jobs: int = 8) -> str:
                 _drain(procs, verbose)
     _drain(procs, verbose)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-ldl"]
         subprocess.run(cmd, check=True)
     return LIB
 

@@ -384,6 +384,9 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 }
 
 // ---- query-centric wpsum ----------------------------------------------------------------
+#ifndef SNLS_WQ_FRAMES
+#define SNLS_WQ_FRAMES 0
+#endif
 // A CTA owns a TY x TX output tile of one frame (all channels).  Phase A: every query whose
 // write set (footprint + stride-cell remainder, aggregate.cpp:80-100) can meet the tile is
 // handled by one group of G lanes (float4 of channels each); for each neighbour l it reads the
@@ -397,7 +400,7 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 // videos (F = 64) split their channels over two CTAs and keep the parked patches, and the
 // shared memory per CTA, at the F = 32 size (two resident CTAs per SM instead of one).
 template <int P, int G, int FG, int TY, int TX>
-__global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
+__global__ void __launch_bounds__(256, 2) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
                                                           int32_t* __restrict__ counts) {
     extern __shared__ float4 s_patch[];  // [query][P*P][G]
     constexpr int HP = P / 2, NQG = 256 / G;
@@ -415,6 +418,41 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
     const int cg0 = int(blockIdx.y) * G;  // first float4 channel group of this CTA
     const float4* vbase = reinterpret_cast<const float4*>(a.v) + cg0 + gl;
 
+#if SNLS_WQ_FRAMES
+    // frame-major phase A: all groups sweep the key frames in the same order, so the CTA's L1
+    // working set is one frame's region at a time (a group owns its queries' parked patches
+    // and adds each frame's partial sums to them: deterministic, no races)
+    for (int qi = grp; qi < nq; qi += NQG) {
+        float4* dst = s_patch + size_t(qi) * P * P * G + gl;
+#pragma unroll
+        for (int i = 0; i < P * P; ++i) dst[i * G] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // pass kf = ti - wt .. ti + wt, then one catch-all pass (kf = -1) for offsets reaching
+    // further than the search's wt (wpsum accepts any in-clip offset, aggregate.cpp:108-109)
+    const int kf_lo = max(0, ti - a.wt), kf_hi = min(a.d.t - 1, ti + a.wt);
+    for (int kp = kf_lo; kp <= kf_hi + 1; ++kp)
+    for (int qi = grp; qi < nq; qi += NQG) {
+        const int kf = kp <= kf_hi ? kp : -1;
+        const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
+        const int qy = gy * st, qx = gx * st;
+        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx - a.d.row0;
+        float4 acc[P][P];
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int j = 0; j < P; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool any = false;
+        for (int l = 0; l < a.topl; ++l) {
+            const size_t e = size_t(row) * a.topl + l;
+            const float* o = a.offsets + e * 3;
+            int kt = ti + int(roundf(__ldg(o)));
+            if (kt < 0 || kt >= a.d.t) {  // "offsets leave the clip" (aggregate.cpp:108-109)
+                if (kf < 0) latch(a.err, kErrWpsum);
+                continue;
+            }
+            if (kf >= 0 ? kt != kf : (kt >= kf_lo && kt <= kf_hi)) continue;
+            any = true;
+#else
     for (int qi = grp; qi < nq; qi += NQG) {
         const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
         const int qy = gy * st, qx = gx * st;
@@ -432,6 +470,7 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
                 latch(a.err, kErrWpsum);
                 kt = ti;
             }
+#endif
             const float oy = __ldg(o + 1), ox = __ldg(o + 2);
             const float fly = floorf(oy), flx = floorf(ox);
             const float fy = oy - fly, fx = ox - flx;
@@ -470,10 +509,23 @@ __global__ void __launch_bounds__(256) wpsum_query_kernel(AggArgs a, float* __re
                 }
         }
         float4* dst = s_patch + size_t(qi) * P * P * G + gl;
+#if SNLS_WQ_FRAMES
+        if (any) {
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    float4& d = dst[(i * P + j) * G];
+                    const float4 v = acc[i][j];
+                    d = make_float4(d.x + v.x, d.y + v.y, d.z + v.z, d.w + v.w);
+                }
+        }
+#else
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int j = 0; j < P; ++j) dst[(i * P + j) * G] = acc[i][j];
+#endif
     }
     __syncthreads();
 

@@ -579,7 +579,7 @@ int snls_wpsum_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
     if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "wpsum: empty or invalid frame range");
     DeviceGuard g(ctx->device);
     AggArgs a{v, weights, offsets, restrict_frames(make_dims(dims, cfg->stride0), t0, t1), cfg->ps,
-              cfg->topl, ctx->err};
+              cfg->topl, ctx->err, cfg->wt};
     return after_launch(ctx, launch_wpsum(a, out, counts, ctx->stream), "snls_wpsum_fwd");
 }
 
@@ -588,7 +588,7 @@ int snls_gather_stack(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, con
     if (int rc = agg_checks(ctx, cfg, dims, v, weights, offsets)) return rc;
     if (!out) return fail(SNLS_EARG, "gather_stack: null output");
     DeviceGuard g(ctx->device);
-    AggArgs a{v, weights, offsets, make_dims(dims, cfg->stride0), cfg->ps, cfg->topl, ctx->err};
+    AggArgs a{v, weights, offsets, make_dims(dims, cfg->stride0), cfg->ps, cfg->topl, ctx->err, cfg->wt};
     return after_launch(ctx, launch_gather_stack(a, out, ctx->stream), "snls_gather_stack");
 }
 
@@ -613,7 +613,7 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     cudaMemsetAsync(dv, 0, size_t(dims.t) * dims.h * dims.w * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dw, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
-    AggArgs a{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err};
+    AggArgs a{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err, cfg->wt};
     return after_launch(ctx, launch_wpsum_bwd(a, grad_out, counts, dv, dw, ctx->stream), "snls_wpsum_bwd");
 }
 

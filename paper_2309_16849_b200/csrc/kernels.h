@@ -44,6 +44,8 @@ struct AggArgs {
     Dims d;
     int ps, topl;
     int* err;
+    int wt;  // the search's temporal radius: a hint for frame-ordered traversals (offsets
+             // reaching further are still served)
 };
 
 int launch_flows_check(const float* ff, const float* bf, int64_t n, int* err, cudaStream_t st);

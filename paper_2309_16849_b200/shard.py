@@ -1,17 +1,25 @@
-"""Frame sharding of one video across ranks (BASELINE configs[4]).
+"""Frame sharding of one video across GPUs (BASELINE configs[4]):
+a thin ctypes wrapper over the C-ABI's shard plan and NCCL halo exchange
+(csrc/comm.cu, include/snls_cuda.h) -- no torch.distributed on the data path.
 
 A query at frame t only reads key/value frames t-wt .. t+wt and the flow frames between
 (search.cpp:84-101, 300), and wpsum writes only into the query's own frame
 (aggregate.cpp:197-198).  So rank r owns query frames [a, b) and needs the slab
 [lo, hi) = [a-wt, b+wt) ∩ [0, T) of K/V/flows: the wt-frame halo on each side comes from the
-neighbouring owners by point-to-point send/recv -- NCCL over NVLink on GPUs, gloo in the
-CPU tests -- and no other collective touches the data path.  Searching the slab with query
-rows restricted to [a-lo, b-lo) (snls_search_fwd_frames) gives exactly the rows the
-unsharded search gives: frames outside the slab are either off the clip or out of reach.
+neighbouring owners by ncclSend/ncclRecv over NVLink.  Searching the slab with query rows
+restricted to [a-lo, b-lo) (snls_search_fwd_frames) gives exactly the rows the unsharded
+search gives: frames outside the slab are either off the clip or out of reach.
+
+torch tensors are only the device buffers here; torch.distributed is used once, as the
+out-of-band channel that hands rank 0's NCCL id to the other ranks (Comm.create).
+The CPU tests run the same plan with a gloo stand-in exchange (tests/shard_gloo.py).
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
+
+from . import snls as S
 
 
 @dataclass(frozen=True)
@@ -34,76 +42,45 @@ class ShardPlan:
         return self.b - self.lo
 
 
-def owned_range(T: int, world: int, rank: int):
-    """Balanced contiguous split of T frames over `world` ranks."""
-    per, rem = divmod(T, world)
-    a = rank * per + min(rank, rem)
-    return a, a + per + (1 if rank < rem else 0)
+def _lib():
+    L = S.lib()
+    if not getattr(L, "_snls_comm_types", False):
+        I, P = C.c_int, C.c_void_p
+        L.snls_shard_plan.argtypes = [I, I, I, I, C.POINTER(I)]
+        L.snls_shard_transfers.argtypes = [I, I, I, I, I] + [C.POINTER(I)] * 5
+        L.snls_comm_unique_id.argtypes = [P]
+        L.snls_comm_init.argtypes = [P, P, I, I, C.POINTER(P)]
+        L.snls_comm_destroy.argtypes = [P]
+        L.snls_comm_info.argtypes = [P, C.POINTER(I), C.POINTER(I)]
+        L.snls_halo_exchange_async.argtypes = [P, I, I, I, C.POINTER(P), C.POINTER(C.c_int64)]
+        L.snls_halo_wait.argtypes = [P]
+        L.snls_reverse_halo_add.argtypes = [P, I, I, I, C.POINTER(P), C.POINTER(C.c_int64)]
+        L.snls_comm_loopback.argtypes = [P, P, P, C.c_uint64]
+        L._snls_comm_types = True
+    return L
 
 
 def plan(T: int, world: int, rank: int, wt: int) -> ShardPlan:
-    if world > T:
-        raise ValueError("frame sharding needs at least one frame per rank")
-    a, b = owned_range(T, world, rank)
-    return ShardPlan(rank, world, T, wt, a, b, max(0, a - wt), min(T, b + wt))
+    """snls_shard_plan: balanced contiguous split; slab = owned frames +- wt, clipped."""
+    out = (C.c_int * 4)()
+    S._raise(_lib().snls_shard_plan(T, world, rank, wt, out))
+    return ShardPlan(rank, world, T, wt, out[0], out[1], out[2], out[3])
+
+
+def owned_range(T: int, world: int, rank: int):
+    p = plan(T, world, rank, 0)
+    return p.a, p.b
 
 
 def transfers(p: ShardPlan):
-    """(peer, frame range, 'send'|'recv') messages of rank p.rank, peers in ascending order.
-    A peer's frames that fall in my slab are received; my frames inside a peer's slab are sent.
-    Works for any shard length (halo may span several owners when b - a < wt)."""
-    out = []
-    for peer in range(p.world):
-        if peer == p.rank:
-            continue
-        pa, pb = owned_range(p.T, p.world, peer)
-        # frames I need from `peer`
-        lo, hi = max(p.lo, pa), min(p.hi, pb)
-        if lo < hi:
-            out.append((peer, (lo, hi), "recv"))
-        # frames `peer` needs from me
-        q = plan(p.T, p.world, peer, p.wt)
-        lo, hi = max(q.lo, p.a), min(q.hi, p.b)
-        if lo < hi:
-            out.append((peer, (lo, hi), "send"))
-    return out
-
-
-def exchange(local, p: ShardPlan, group=None):
-    """Assemble the slab [lo, hi) from `local` (the owned frames [a, b), frame-major tensor)
-    with one batched send/recv per (peer, direction).  Returns the slab tensor."""
-    import torch
-    import torch.distributed as dist
-
-    shape = (p.hi - p.lo,) + tuple(local.shape[1:])
-    slab = torch.empty(shape, dtype=local.dtype, device=local.device)
-    slab[p.a - p.lo:p.b - p.lo].copy_(local)
-    ops = []
-    for peer, (lo, hi), kind in transfers(p):
-        if kind == "recv":
-            ops.append(dist.P2POp(dist.irecv, slab[lo - p.lo:hi - p.lo], peer, group))
-        else:
-            ops.append(dist.P2POp(dist.isend, local[lo - p.a:hi - p.a].contiguous(), peer, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    return slab
-
-
-def exchange_async(slabs, p: ShardPlan, group=None):
-    """Fill the halo frames of persistent slab tensors in place: every tensor in `slabs` is a
-    frame-major [lo, hi) slab whose owned frames [a, b) are already in place; one batched
-    send/recv per (peer, direction, tensor) is started and the work handles are returned
-    (NCCL: wait() only orders the caller's stream after the transfer, so work enqueued
-    before it -- the interior frames -- overlaps the exchange)."""
-    import torch.distributed as dist
-
-    ops = []
-    for slab in slabs:
-        for peer, (lo, hi), kind in transfers(p):
-            view = slab[lo - p.lo:hi - p.lo]
-            ops.append(dist.P2POp(dist.irecv if kind == "recv" else dist.isend, view, peer, group))
-    return dist.batch_isend_irecv(ops) if ops else []
+    """(peer, (lo, hi), 'recv'|'send') messages of rank p.rank (snls_shard_transfers): a
+    peer's frames inside my slab are received, my frames inside a peer's slab are sent;
+    peers ascending, recv before send.  Any shard length (a halo may span several owners)."""
+    cap = 4 * p.world + 4
+    arr = [(C.c_int * cap)() for _ in range(4)]
+    n = C.c_int()
+    S._raise(_lib().snls_shard_transfers(p.T, p.world, p.rank, p.wt, cap, *arr, C.byref(n)))
+    return [(arr[0][i], (arr[1][i], arr[2][i]), "recv" if arr[3][i] else "send") for i in range(n.value)]
 
 
 def interior_range(p: ShardPlan):
@@ -115,21 +92,94 @@ def interior_range(p: ShardPlan):
     return lo, hi
 
 
-def search_aggregate_overlapped(slab_q, slab_k, slab_v, slab_ff, slab_bf, p: ShardPlan, cfg, out,
-                                ctx=None, group=None, world=1, split=None):
-    """One frame-sharded step with the halo exchange overlapped: start the exchange of the
-    K/V/flow halo, search + aggregate the interior frames (no halo needed) meanwhile, wait,
-    then do the edge frames.  `out` = (sims, offsets, chains, weights, video, counts) for
-    the owned frames; the slabs are persistent [lo, hi) tensors with the owned frames in
-    place (Q only needs its owned frames)."""
-    from . import snls as S
+class Comm:
+    """An NCCL communicator of the C-ABI (snls_comm) bound to a context's device/stream."""
 
+    def __init__(self, unique_id: bytes, rank: int, world: int, ctx=None):
+        import torch
+
+        self.ctx = ctx or S.context(torch.cuda.current_device())
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        S._raise(_lib().snls_comm_init(self.ctx.h, buf, rank, world, C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        S._raise(_lib().snls_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def create(cls, rank: int, world: int, ctx=None):
+        """Rank 0 makes the id; torch.distributed (already initialised) carries it to the
+        other ranks -- the only use of torch.distributed here (control plane)."""
+        uid = cls.unique_id() if rank == 0 else None
+        if world > 1:
+            import torch.distributed as dist
+
+            box = [uid]
+            dist.broadcast_object_list(box, src=0)
+            uid = box[0]
+        return cls(uid, rank, world, ctx)
+
+    def info(self):
+        n, v = C.c_int(), C.c_int()
+        S._raise(_lib().snls_comm_info(self.h, C.byref(n), C.byref(v)))
+        return {"nranks": n.value, "nccl_version": v.value}
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().snls_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _arrays(tensors, per_frame):
+        n = len(tensors)
+        ptrs = (C.c_void_p * max(n, 1))(*[S._ptr(t).value for t in tensors])
+        sizes = (C.c_int64 * max(n, 1))(*[per_frame(t) for t in tensors])
+        return n, ptrs, sizes
+
+    def exchange_async(self, slabs, p: ShardPlan):
+        """snls_halo_exchange_async on persistent [lo, hi) slabs (owned frames in place)."""
+        n, ptrs, sizes = self._arrays(slabs, lambda t: t[0].numel() * t.element_size())
+        S._raise(_lib().snls_halo_exchange_async(self.h, p.T, p.wt, n, ptrs, sizes))
+
+    def wait(self):
+        S._raise(_lib().snls_halo_wait(self.h))
+
+    def reverse_add(self, slab_grads, p: ShardPlan):
+        """snls_reverse_halo_add: halo partial gradients to their owners, owned frames += the
+        peers' partial sums (in place)."""
+        n, ptrs, sizes = self._arrays(slab_grads, lambda t: t[0].numel())
+        S._raise(_lib().snls_reverse_halo_add(self.h, p.T, p.wt, n, ptrs, sizes))
+
+    def loopback(self, src, dst):
+        S._raise(_lib().snls_comm_loopback(self.h, S._ptr(src), S._ptr(dst),
+                                           src.numel() * src.element_size()))
+
+
+def search_aggregate_overlapped(slab_q, slab_k, slab_v, slab_ff, slab_bf, p: ShardPlan, cfg, out,
+                                ctx=None, comm: Comm | None = None, split=None):
+    """One frame-sharded step with the halo exchange overlapped: start the NCCL exchange of
+    the K/V/flow halo, search + aggregate the interior frames (no halo needed) meanwhile,
+    join, then do the edge frames.  `out` = (sims, offsets, chains, weights, video, counts)
+    for the owned frames; the slabs are persistent [lo, hi) tensors with the owned frames in
+    place (Q only needs its owned frames)."""
     sims, offs, chains, wts, vout, counts = out
     uniq = []  # aliased slabs (Q = K = V) are exchanged once
     for x in (slab_k, slab_v, slab_ff, slab_bf):
         if all(x is not u for u in uniq):
             uniq.append(x)
-    reqs = exchange_async(uniq, p, group) if world > 1 else []
+    if comm is not None:
+        comm.exchange_async(uniq, p)
     nq = sims.shape[0] // (p.b - p.a)
 
     def run(f0, f1):  # owned query frames [f0, f1)
@@ -142,56 +192,28 @@ def search_aggregate_overlapped(slab_q, slab_k, slab_v, slab_ff, slab_bf, p: Sha
         S.wpsum(slab_v, wts[r0:r1], offs[r0:r1], cfg, ctx=ctx, check=False,
                 out=(vout[f0 - p.a:f1 - p.a], counts[f0 - p.a:f1 - p.a]), frames=(f0 - p.lo, f1 - p.lo))
 
-    split = world > 1 if split is None else split
+    split = comm is not None if split is None else split
     ia, ib = interior_range(p) if split else (p.a, p.b)
     run(ia, ib)
-    for r in reqs:
-        r.wait()
+    if comm is not None:
+        comm.wait()
     run(p.a, ia)
     run(ib, p.b)
 
 
-def reverse_exchange_add(slab_grads, p: ShardPlan, group=None):
-    """The backward's halo step: gradients a rank accumulated into its
-    halo frames (dK / dV / dFlow land in frames qt + dt, search.cpp:584-666;
-    aggregate.cpp:412-460) belong to the owners of those frames.  Every halo range received
-    in the forward is sent back; every range sent in the forward comes back from that peer
-    as a partial sum and is added into the owned frames.  In place on the slab tensors;
-    afterwards each rank's owned frames [t0, t1) hold the full gradient."""
-    import torch
-    import torch.distributed as dist
-
-    ops, pending = [], []
-    for g in slab_grads:
-        for peer, (lo, hi), kind in transfers(p):
-            view = g[lo - p.lo:hi - p.lo]
-            if kind == "recv":  # my partial sums for the peer's frames go back to it
-                ops.append(dist.P2POp(dist.isend, view.contiguous(), peer, group))
-            else:  # the peer's partial sums for my frames
-                buf = torch.empty_like(view)
-                ops.append(dist.P2POp(dist.irecv, buf, peer, group))
-                pending.append((view, buf))
-    for r in (dist.batch_isend_irecv(ops) if ops else []):
-        r.wait()
-    for view, buf in pending:
-        view.add_(buf)
-
-
 def backward_shard(grad_sims, grad_out, res, counts, slab_q, slab_k, slab_v, p: ShardPlan, cfg,
-                   ctx=None, group=None, world=1):
+                   ctx=None, comm: Comm | None = None):
     """wpsum_backward + shifted_nls_backward for the owned rows/frames of a frame shard
-    (frame-range entry points on the slab), then the reverse halo exchange.  Returns
-    slab-shaped (dq, dk, dv, dfflow, dbflow) whose owned frames hold the full gradient
-    (Q's halo frames carry nothing: queries read only their own frame), and dweights."""
-    from . import snls as S
-
+    (frame-range entry points on the slab), then the reverse halo (snls_reverse_halo_add).
+    Returns slab-shaped (dq, dk, dv, dfflow, dbflow) whose owned frames hold the full
+    gradient (Q's halo frames carry nothing: queries read only their own frame), and dW."""
     fr = (p.t0, p.t1)
     dv, dw = S.wpsum_backward(grad_out, counts, slab_v, res.weights, res.offsets, cfg, ctx=ctx,
                               check=False, frames=fr)
     dq, dk, dff, dbf = S.shifted_nls_backward(grad_sims, res, slab_q, slab_k, ctx=ctx, check=False,
                                               frames=fr)
-    if world > 1:
-        reverse_exchange_add([dk, dv, dff, dbf], p, group)
+    if comm is not None and p.world > 1:
+        comm.reverse_add([dk, dv, dff, dbf], p)
     return dq, dk, dv, dff, dbf, dw
 
 
@@ -200,8 +222,6 @@ def search_aggregate_shard(q_local, k_slab, v_slab, ff_slab, bf_slab, p: ShardPl
     """Search + fused softmax + wpsum for the owned frames on the device (C-ABI frame-range
     entry points).  q_local holds the owned frames only; Q's halo is never read."""
     import torch
-
-    from . import snls as S
 
     q_slab = q_local
     if q_local.shape[0] != k_slab.shape[0]:

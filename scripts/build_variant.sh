@@ -11,5 +11,5 @@ tmp=$(mktemp -d)
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
   --expt-relaxed-constexpr -I "$root/include" -I "$pkg/csrc" "$@" -c "${SRC:-$pkg/csrc/${UNIT:-search_tiled}.cu}" -o "$tmp/${UNIT:-search_tiled}.o"
 objs=$(ls "$pkg"/build/*.o | grep -v ${UNIT:-search_tiled}.o)
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" $objs "$tmp/${UNIT:-search_tiled}.o" -cudart static
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" $objs "$tmp/${UNIT:-search_tiled}.o" -cudart static -ldl
 rm -rf "$tmp"

@@ -73,7 +73,7 @@ def test_overlapped_interior_then_edges_equals_unsharded(world):
 def test_frame_range_backward_plus_reverse_halo_equals_unsharded(world):
     """Each rank runs wpsum_backward + shifted_nls_backward on its slab for its own rows
     (frame-range entry points); adding every rank's slab gradients into the clip -- what
-    reverse_exchange_add does over NCCL -- gives the unsharded device gradients (fp32
+    snls_reverse_halo_add does over NCCL -- gives the unsharded device gradients (fp32
     atomics in a different order: REL_TOL)."""
     import torch
 
@@ -107,3 +107,41 @@ def test_frame_range_backward_plus_reverse_halo_equals_unsharded(world):
             a_[p.lo:p.hi] += g
     for a_, w in zip(acc, (want[0], want[1], want_dv, want[2], want[3])):
         assert max_rel(host(a_), host(w)) <= REL_TOL
+
+
+def test_nccl_communicator_world1_selfcheck():
+    """The C-ABI's own NCCL communicator on the lease's single GPU: ncclCommInitRank over a
+    fresh id, ncclCommCount == 1, a grouped ncclSend/ncclRecv to itself moves the bytes, the
+    halo exchange and reverse halo are no-ops at world 1 (no peers), and the overlapped step
+    through the communicator equals the plain step."""
+    import torch
+
+    S = snls_mod()
+    P = Checker("port")
+    comm = shard.Comm(shard.Comm.unique_id(), 0, 1)
+    info = comm.info()
+    assert info["nranks"] == 1 and info["nccl_version"] > 0
+    src = torch.arange(1 << 20, device="cuda", dtype=torch.float32)
+    dst = torch.zeros_like(src)
+    comm.loopback(src, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(src, dst)
+    T, H, W, F = 6, 16, 16, 32
+    cfg = S.SearchConfig(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2", softmax_scale=1 / 288)
+    v = dev(video(P, T, H, W, F, 41))
+    ff, bf = dev(flow(P, T, H, W, 42, 2.0)), dev(flow(P, T, H, W, 43, 2.0))
+    p = shard.plan(T, 1, 0, cfg.wt)
+    assert shard.transfers(p) == []
+    nq = ((H - 1) // 2 + 1) * ((W - 1) // 2 + 1)
+    o = (torch.empty((T * nq, 10), device="cuda"), torch.empty((T * nq, 10, 3), device="cuda"), None,
+         torch.empty((T * nq, 10), device="cuda"), torch.empty((T, H, W, F), device="cuda"),
+         torch.empty((T, H, W), device="cuda", dtype=torch.int32))
+    shard.search_aggregate_overlapped(v, v, v, ff, bf, p, cfg, o, comm=comm, split=True)
+    full = S.shifted_nls_forward(v, v, ff, bf, cfg, want_weights=True)
+    fout, _ = S.wpsum(v, full.weights, full.offsets, cfg)
+    assert torch.equal(o[0], full.sims) and torch.equal(o[4], fout)
+    g = torch.ones_like(v)
+    comm.reverse_add([g], p)
+    torch.cuda.synchronize()
+    assert torch.equal(g, torch.ones_like(v))
+    comm.close()

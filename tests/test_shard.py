@@ -1,8 +1,8 @@
 """CPU (gloo, world size 2 and 3): frame sharding with a wt-frame halo.
 
 Each rank owns a contiguous frame range, assembles its slab [a-wt, b+wt) ∩ [0, T) through
-paper_2309_16849_b200.shard.exchange (batched point-to-point send/recv -- NCCL on the GPU
-box, gloo here), and computes its rows on the slab.  With the oracle as the compute the
+the shard plan of the C-ABI (snls_shard_plan / snls_shard_transfers) moved by a gloo
+stand-in of the NCCL exchange (tests/shard_gloo.py), and computes its rows on the slab.  With the oracle as the compute the
 sharded rows must equal the unsharded ones BIT FOR BIT: that pins the halo plan, the
 exchange and the frame-range semantics the CUDA entry points (snls_*_frames) implement."""
 import os
@@ -51,6 +51,7 @@ def _worker(rank, world, port, T, out_dir):
 
     from oracle.oracle import Cfg, Checker
     from paper_2309_16849_b200 import shard as SH
+    from tests import shard_gloo as G
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
@@ -65,9 +66,9 @@ def _worker(rank, world, port, T, out_dir):
     own_v = torch.tensor(np.stack([frame(t, 500, -1, 1, F) for t in range(p.a, p.b)]).astype(np.float32))
     own_ff = torch.tensor(np.stack([frame(t, 501, -1.5, 1.5, 2) for t in range(p.a, p.b)]).astype(np.float32))
     own_bf = torch.tensor(np.stack([frame(t, 502, -1.5, 1.5, 2) for t in range(p.a, p.b)]).astype(np.float32))
-    v = SH.exchange(own_v, p).double().numpy()
-    ff = SH.exchange(own_ff, p).double().numpy()
-    bf = SH.exchange(own_bf, p).double().numpy()
+    v = G.exchange(own_v, p).double().numpy()
+    ff = G.exchange(own_ff, p).double().numpy()
+    bf = G.exchange(own_bf, p).double().numpy()
     res = P.search_fwd(v, v, ff, bf, cfg)          # Q = K = V, slab as a clip
     nq = ((H - 1) // cfg.stride0 + 1) * ((W - 1) // cfg.stride0 + 1)
     rows = slice(p.t0 * nq, p.t1 * nq)
@@ -132,6 +133,7 @@ def _async_worker(rank, world, port, T, out_dir):
     import torch.distributed as dist
 
     from paper_2309_16849_b200 import shard as SH
+    from tests import shard_gloo as G
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
@@ -141,8 +143,7 @@ def _async_worker(rank, world, port, T, out_dir):
     slab[p.t0:p.t1] = full[p.a:p.b]
     flow = torch.full((p.hi - p.lo, 3, 2), -2.0)
     flow[p.t0:p.t1] = -full[p.a:p.b]
-    for r in SH.exchange_async([slab, flow], p):
-        r.wait()
+    G.exchange_inplace([slab, flow], p)
     np.savez(os.path.join(out_dir, f"a{rank}.npz"), slab=slab.numpy(), flow=flow.numpy(),
              want=full[p.lo:p.hi].numpy())
     dist.barrier()
@@ -170,6 +171,7 @@ def _bwd_worker(rank, world, port, T, out_dir):
 
     from oracle.oracle import Cfg, Checker
     from paper_2309_16849_b200 import shard as SH
+    from tests import shard_gloo as G
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
@@ -192,7 +194,7 @@ def _bwd_worker(rank, world, port, T, out_dir):
     dv, _ = P.wpsum_bwd(g_o, counts, sv, wts, res["offsets"], cfg)
     gb = P.search_bwd(sv, sv, cfg, res["centers"], res["chains"], g_s)
     grads = [torch.tensor(x) for x in (gb["dk"], dv, gb["dfflow"], gb["dbflow"])]
-    SH.reverse_exchange_add(grads, p)
+    G.reverse_exchange_add(grads, p)
     np.savez(os.path.join(out_dir, f"b{rank}.npz"), dq=gb["dq"][p.t0:p.t1],
              **{n: g[p.t0:p.t1].numpy() for n, g in zip(("dk", "dv", "dff", "dbf"), grads)},
              a=p.a, b=p.b)
@@ -233,3 +235,47 @@ def test_gloo_reverse_halo_backward_matches_unsharded_oracle(tmp_path, world, T)
         a, b = int(z["a"]), int(z["b"])
         for n, w in want.items():  # fp64, summation order differs: tight tolerance
             assert np.allclose(z[n], w[a:b], rtol=1e-12, atol=1e-12), n
+
+
+def _py_plan(T, world, rank, wt):
+    """Independent restatement of the plan for checking the C-ABI's."""
+    per, rem = divmod(T, world)
+    a = rank * per + min(rank, rem)
+    b = a + per + (1 if rank < rem else 0)
+    return a, b, max(0, a - wt), min(T, b + wt)
+
+
+def test_c_abi_plan_matches_independent_restatement():
+    for T in (1, 5, 8, 13, 64):
+        for world in (1, 2, 3, 4, 8):
+            if world > T:
+                with pytest.raises(Exception, match="at least one frame"):
+                    shard.plan(T, world, 0, 2)
+                continue
+            for wt in (0, 1, 2, 3):
+                for r in range(world):
+                    p = shard.plan(T, world, r, wt)
+                    assert (p.a, p.b, p.lo, p.hi) == _py_plan(T, world, r, wt)
+                    want = []
+                    for peer in range(world):
+                        if peer == r:
+                            continue
+                        pa, pb, _, _ = _py_plan(T, world, peer, wt)
+                        lo, hi = max(p.lo, pa), min(p.hi, pb)
+                        if lo < hi:
+                            want.append((peer, (lo, hi), "recv"))
+                        _, _, qlo, qhi = _py_plan(T, world, peer, wt)
+                        lo, hi = max(qlo, p.a), min(qhi, p.b)
+                        if lo < hi:
+                            want.append((peer, (lo, hi), "send"))
+                    assert shard.transfers(p) == want
+
+
+def test_comm_api_is_exported():
+    from paper_2309_16849_b200 import snls as S
+
+    L = S.lib()
+    for name in ("snls_comm_unique_id", "snls_comm_init", "snls_comm_destroy", "snls_comm_info",
+                 "snls_halo_exchange_async", "snls_halo_wait", "snls_reverse_halo_add",
+                 "snls_comm_loopback", "snls_shard_plan", "snls_shard_transfers"):
+        assert hasattr(L, name), name

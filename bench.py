@@ -535,6 +535,8 @@ def run_ours(args, wl):
         "clocks": clk,
         "wall_s_timed_loop": wall,
     }
+    if world == 1 and not wl.get("sharded") and not wl.get("train"):
+        result["e2e_cpp_api"] = cpp_api_e2e(wl)
     if world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
     print(json.dumps(result), flush=True)
@@ -582,6 +584,28 @@ def reference_sample(wl, crop):
         return time.perf_counter() - t0
 
     return R, rows, run
+
+
+def cpp_api_e2e(wl):
+    """The reference's own C++ caller, snls::run_benchmark (harness.cpp:242-283), timing
+    snls::shifted_nls_forward through the C++ drop-in (host/build/bench_gpu: libsnls_gpu.so
+    over libsnls_cuda.so) on this workload's shape: fp64 host containers in and out, the
+    conversions and copies inside the timed region (search only -- run_benchmark times the
+    forward)."""
+    exe = os.path.join(ROOT, "paper_2309_16849_b200", "host", "build", "bench_gpu")
+    if not os.path.exists(exe):
+        return {"unavailable": "host/build/bench_gpu not built (needs the reference headers)"}
+    args = [str(x) for x in (wl["T"], wl["H"], wl["W"], wl["C"], wl["ws"], wl["wt"], wl["ps"],
+                             wl["stride0"], wl["topl"], wl["metric"], 5)]
+    try:
+        p = subprocess.run([exe] + args, capture_output=True, text=True, timeout=600)
+        r = json.loads(p.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal
+        return {"unavailable": f"bench_gpu failed: {e}"}
+    return {"value": r["queries_per_s"], "unit": UNIT, "ms_per_video": r["median_ms"],
+            "api": "snls::shifted_nls_forward (reference C++ API; snls::run_benchmark, median of 5) "
+                   "through libsnls_gpu.so -> libsnls_cuda.so, fp64 containers in/out",
+            "ok": r["ok"]}
 
 
 def cpu_model():

@@ -103,6 +103,15 @@ int snls_device_free(snls_ctx* ctx, void* ptr);
 /* Stream-ordered copies; snls_copy_d2h returns after the data has landed. */
 int snls_copy_h2d(snls_ctx* ctx, void* dst_device, const void* src_host, uint64_t bytes);
 int snls_copy_d2h(snls_ctx* ctx, void* dst_host, const void* src_device, uint64_t bytes);
+/* Stream-ordered copy that does not wait (kind 1 H2D, 2 D2H, 3 D2D; pinned host memory for
+ * true asynchrony), and events on the context's stream, so C++ callers can pipeline host
+ * work against transfers without CUDA headers. */
+int snls_copy_async(snls_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
+typedef struct snls_event snls_event;
+int snls_event_create(snls_ctx* ctx, snls_event** out);
+int snls_event_record(snls_ctx* ctx, snls_event* ev);
+int snls_event_sync(snls_event* ev);
+int snls_event_destroy(snls_event* ev);
 
 /* ---- search (search.hpp) ------------------------------------------------------------ */
 /* Replaces snls::shifted_nls_forward (search.hpp:126-128; search.cpp:414-421).
@@ -180,6 +189,14 @@ int snls_search_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, in
 int snls_search_tape64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
                        const float* fflow, const float* bflow, const float* offsets,
                        double* centers, double* chains64);
+/* The whole SearchResult in the reference's fp64 layout from one device result (the C++
+ * drop-in downloads these directly): sims64 = double(sims), offsets64 = (dt, ky-qy, kx-qx)
+ * and centres / chains as snls_search_tape64 (exact fp64 positions).  Any fp64 output may
+ * be NULL. */
+int snls_search_results64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* fflow, const float* bflow, const float* sims,
+                          const float* offsets, double* sims64, double* offsets64,
+                          double* centers, double* chains64);
 
 /* ---- frame sharding across GPUs: shard plan + NCCL halos -------
  * One video of T frames over `world` ranks: rank r owns query frames [a, b) (balanced

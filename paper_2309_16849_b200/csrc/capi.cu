@@ -336,6 +336,67 @@ int snls_copy_d2h(snls_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
     return SNLS_OK;
 }
 
+// Stream-ordered copy without a host wait (kind 1 H2D, 2 D2H, 3 D2D); host buffers should be
+// pinned (snls_host_register) for the copy to be asynchronous.
+int snls_copy_async(snls_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (bytes == 0) return SNLS_OK;
+    if (!dst || !src) return fail(SNLS_EARG, "snls_copy_async: null pointer");
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost
+                           : kind == 3 ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault;
+    if (kind < 1 || kind > 3) return fail(SNLS_EARG, "snls_copy_async: kind must be 1, 2 or 3");
+    DeviceGuard g(ctx->device);
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, k, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_copy_async");
+    return SNLS_OK;
+}
+
+struct snls_event {
+    cudaEvent_t ev = nullptr;
+    int device = 0;
+};
+
+int snls_event_create(snls_ctx* ctx, snls_event** out) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (!out) return fail(SNLS_EARG, "snls_event_create: null output");
+    DeviceGuard g(ctx->device);
+    auto* ev = new snls_event();
+    ev->device = ctx->device;
+    const cudaError_t e = cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        delete ev;
+        return cuda_fail(e, "snls_event_create");
+    }
+    *out = ev;
+    return SNLS_OK;
+}
+
+int snls_event_record(snls_ctx* ctx, snls_event* ev) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (!ev) return fail(SNLS_EARG, "snls_event_record: null event");
+    DeviceGuard g(ctx->device);
+    const cudaError_t e = cudaEventRecord(ev->ev, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_event_record");
+    return SNLS_OK;
+}
+
+int snls_event_sync(snls_event* ev) {
+    if (!ev) return fail(SNLS_EARG, "snls_event_sync: null event");
+    DeviceGuard g(ev->device);
+    const cudaError_t e = cudaEventSynchronize(ev->ev);
+    if (e != cudaSuccess) return cuda_fail(e, "snls_event_sync");
+    return SNLS_OK;
+}
+
+int snls_event_destroy(snls_event* ev) {
+    if (!ev) return SNLS_OK;
+    DeviceGuard g(ev->device);
+    cudaEventDestroy(ev->ev);
+    delete ev;
+    return SNLS_OK;
+}
+
 static int search_common_checks(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                                 const float* q, const float* k, const float* ff, const float* bf) {
     if (int rc = check_ctx(ctx)) return rc;
@@ -528,20 +589,29 @@ int snls_search_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, in
 int snls_search_tape64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
                        const float* ff, const float* bf, const float* offsets, double* centers,
                        double* chains64) {
+    if (!centers) return fail(SNLS_EARG, "search_tape64: null tensor");
+    return snls_search_results64(ctx, cfg, dims, t0, t1, ff, bf, nullptr, offsets, nullptr, nullptr,
+                                 centers, chains64);
+}
+
+int snls_search_results64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                          const float* ff, const float* bf, const float* sims, const float* offsets,
+                          double* sims64, double* offsets64, double* centers, double* chains64) {
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = validate(cfg)) return rc;
     if (int rc = check_dims(dims)) return rc;
     if ((ff == nullptr) != (bf == nullptr))
         return fail(SNLS_EARG, "search: pass both flows or neither (nls_forward)");
-    if (!offsets || !centers) return fail(SNLS_EARG, "search_tape64: null tensor");
-    if (cfg->wt > 1 && !chains64) return fail(SNLS_EARG, "search_tape64: the tape needs chains when wt > 1");
-    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "search_tape64: empty or invalid frame range");
+    if (!offsets) return fail(SNLS_EARG, "search_results64: null offsets");
+    if (sims64 && !sims) return fail(SNLS_EARG, "search_results64: sims64 needs sims");
+    if (chains64 && cfg->wt <= 1) chains64 = nullptr;
+    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "search_results64: empty or invalid frame range");
     DeviceGuard g(ctx->device);
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     return after_launch(ctx,
                         launch_tape64(ff, bf, d, cfg->ws, cfg->wt, cfg->topl, cfg->stride1, offsets,
-                                      centers, cfg->wt > 1 ? chains64 : nullptr, ctx->stream),
-                        "snls_search_tape64");
+                                      centers, chains64, sims, sims64, offsets64, ctx->stream),
+                        "snls_search_results64");
 }
 
 int snls_softmax_rows(snls_ctx* ctx, int64_t rows, int l, double beta, const float* sims, float* weights) {

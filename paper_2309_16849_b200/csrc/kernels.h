@@ -60,7 +60,8 @@ int launch_topl(int64_t rows, int cols, const float* full, const float* full_off
 int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,
                      const float* offsets, float* chains, cudaStream_t st);
 int launch_tape64(const float* ff, const float* bf, Dims d, int ws, int wt, int topl, double stride1,
-                  const float* offsets, double* centers, double* chains, cudaStream_t st);
+                  const float* offsets, double* centers, double* chains, const float* sims,
+                  double* sims64, double* offsets64, cudaStream_t st);
 int launch_replay(const float* q, const float* k, Dims d, int ps, int metric, int topl,
                   const float* offsets, float* sims, cudaStream_t st);
 

@@ -292,7 +292,8 @@ __global__ void emit_tape_kernel(const float* ff, const float* bf, Dims d, int w
 // window index dyi recovered from the fp32 offset (its rounding is far below stride1 / 2).
 __global__ void tape64_kernel(const float* ff, const float* bf, Dims d, int ws, int wt, int topl,
                               double stride1, const float* offsets, double* centers,
-                              double* chains) {
+                              double* chains, const float* sims, double* sims64,
+                              double* offsets64) {
     const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= d.rows * topl) return;
     const int64_t row = e / topl;
@@ -309,10 +310,20 @@ __global__ void tape64_kernel(const float* ff, const float* bf, Dims d, int ws, 
     if (kt >= 0 && kt < d.t) shift_to_t<double>(ff, bf, d.h, d.w, qt, qy, qx, dt, sdy, sdx,
                                                 (dt > 1 || dt < -1) ? lk : nullptr);
     const double ny = rint((double(o[1]) - sdy) / stride1), nx = rint((double(o[2]) - sdx) / stride1);
-    double* c = centers + size_t(e) * 3;
-    c[0] = double(kt);
-    c[1] = (double(qy) + sdy) + stride1 * ny;
-    c[2] = (double(qx) + sdx) + stride1 * nx;
+    const double ky = (double(qy) + sdy) + stride1 * ny, kx = (double(qx) + sdx) + stride1 * nx;
+    if (centers) {
+        double* c = centers + size_t(e) * 3;
+        c[0] = double(kt);
+        c[1] = ky;
+        c[2] = kx;
+    }
+    if (offsets64) {  // emit_row's offsets (search.cpp:222-224): (dt, ky - qy, kx - qx) in fp64
+        double* o64 = offsets64 + size_t(e) * 3;
+        o64[0] = double(dt);
+        o64[1] = ky - double(qy);
+        o64[2] = kx - double(qx);
+    }
+    if (sims64) sims64[e] = double(sims[e]);
 }
 
 // replay_similarities (search.cpp:470-493): one thread per selected entry.
@@ -405,10 +416,11 @@ int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,
 }
 
 int launch_tape64(const float* ff, const float* bf, Dims d, int ws, int wt, int topl, double stride1,
-                  const float* offsets, double* centers, double* chains, cudaStream_t st) {
+                  const float* offsets, double* centers, double* chains, const float* sims,
+                  double* sims64, double* offsets64, cudaStream_t st) {
     const int64_t n = d.rows * topl;
     tape64_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(ff, bf, d, ws, wt, topl, stride1, offsets,
-                                                            centers, chains);
+                                                            centers, chains, sims, sims64, offsets64);
     return 1;
 }
 

@@ -50,4 +50,17 @@ void download_i32(std::vector<std::int32_t>& host, const std::int32_t* dev, std:
 
 snls_config to_abi(const snls::SearchConfig& cfg);
 
+// Pipelined fp64 -> fp32 upload: the host converts chunk i (OpenMP) into one half of a pinned
+// double buffer while chunk i-1's H2D copy runs; returns with every copy enqueued (the
+// buffer reuse is ordered by events, the caller's later kernels by the stream).
+float* upload_async(DeviceBuffer& buf, const double* host, std::uint64_t n);
+// fp64 device data -> std::vector<double>: the vector is sized (zero-filled by std::vector),
+// then filled from pinned staging chunks (D2H of chunk i+1 overlaps the parallel copy of i).
+void download64(std::vector<double>& host, const double* dev, std::uint64_t n);
+// Size a result vector for a bulk fill (transparent huge pages, parallel first touch, then
+// std::vector's zero-fill); download64 calls it, callers may run it ahead on other threads.
+void size_for_fill(std::vector<double>& host, std::uint64_t n);
+// Stage timing for SNLS_ADAPTER_PROFILE=1 (stderr): mark("name") after each stage.
+void profile_mark(const char* stage);
+
 }  // namespace snls::gpu

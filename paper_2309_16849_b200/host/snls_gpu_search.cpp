@@ -7,8 +7,9 @@
 // 175-183), the underfull ConfigError (search.cpp:324-325), result/tape layout
 // (search.hpp:65-116), byte accounting of results (search.cpp:273-276, 340-345).
 // Differences: arithmetic is fp32 on the device (results agree to 1e-5 relative; top-L
-// indices are bit-exact where fp32 sums are exact, e.g. integer-valued videos), and the
-// backward always scatters with atomics (the reference's non-deterministic mode).
+// indices are bit-exact where fp32 sums are exact, e.g. integer-valued videos).  The
+// backward takes the reference's fp64 tape as is and honours ExecPolicy::deterministic
+// (int64 fixed-point accumulation: bitwise reproducible, SNLS_BWD_DETERMINISTIC).
 #include <algorithm>
 #include <cmath>
 #include <thread>
@@ -134,6 +135,7 @@ snls_dims dims_of(const VideoTensor& v) { return snls_dims{v.t, v.h, v.w, v.f}; 
 
 struct SearchBuffers {
     gpu::DeviceBuffer q, k, ff, bf, sims, offsets, chains, grad, dq, dk, dff, dbf;
+    gpu::DeviceBuffer sims64, offs64, cen64, ch64;
 };
 thread_local SearchBuffers t_buf;
 
@@ -147,16 +149,19 @@ void query_base(const QueryGrid& g, std::int64_t row, double& qt, double& qy, do
 
 }  // namespace
 
-SearchResult shifted_nls_forward(const VideoTensor& q, const VideoTensor& k,
-                                 const FlowField& fflow, const FlowField& bflow,
-                                 const SearchConfig& cfg, const ExecPolicy& policy) {
+namespace {
+// fflow / bflow null: nls_forward's zero flows, never materialised or uploaded.
+SearchResult forward_impl(const VideoTensor& q, const VideoTensor& k, const FlowField* fflow,
+                          const FlowField* bflow, const SearchConfig& cfg, const ExecPolicy& policy) {
     // validate_forward_inputs (search.cpp:175-183), same order and messages
     cfg.validate();
     if (!q.same_shape(k)) throw DomainError("search: query and key shapes differ");
-    if (!fflow.matches_video(q.t, q.h, q.w) || !bflow.matches_video(q.t, q.h, q.w))
-        throw DomainError("search: flow shape does not match the video");
-    fflow.require_finite("search fflow");
-    bflow.require_finite("search bflow");
+    if (fflow) {
+        if (!fflow->matches_video(q.t, q.h, q.w) || !bflow->matches_video(q.t, q.h, q.w))
+            throw DomainError("search: flow shape does not match the video");
+        fflow->require_finite("search fflow");
+        bflow->require_finite("search bflow");
+    }
 
     const QueryGrid grid = QueryGrid::over(q.t, q.h, q.w, cfg.stride0);
     const std::int64_t rows = grid.rows();
@@ -182,65 +187,69 @@ SearchResult shifted_nls_forward(const VideoTensor& q, const VideoTensor& k,
     memory::TransientCharge grid_charge(grid_bytes);
 
     snls_ctx* ctx = gpu::context();
-    float* dq = gpu::upload(t_buf.q, q.data);
-    const float* dk = (&q == &k || q.data == k.data) ? dq : gpu::upload(t_buf.k, k.data);
-    float* dff = gpu::upload(t_buf.ff, fflow.data);
-    float* dbf = gpu::upload(t_buf.bf, bflow.data);
+    gpu::profile_mark("forward: validate + shell");
+    // the result vectors (~400 MB of fp64 at c4, std::vector zero-fills them) are prepared on
+    // helper threads while the inputs upload and the kernels run
+    auto prep_chains = [&] { gpu::size_for_fill(res.tape.chains, n_sel * cs * 6); };
+    auto prep_small = [&] {
+        gpu::size_for_fill(res.tape.centers, n_sel * 3);
+        gpu::size_for_fill(res.offsets.data, n_sel * 3);
+        gpu::size_for_fill(res.sims.values, n_sel);
+    };
+    std::vector<std::thread> prep;
+    const bool big = n_sel * (7 + std::uint64_t(cs) * 6) * sizeof(double) >= (std::uint64_t(64) << 20);
+    if (big) {  // (threads only pay off for large results)
+        prep.emplace_back(prep_chains);
+        prep.emplace_back(prep_small);
+    }
+    // inputs: fp64 -> fp32 conversion pipelined against the H2D copies (Q = K aliased once)
+    const bool alias = (&q == &k || q.data == k.data);
+    float* dq = gpu::upload_async(t_buf.q, q.data.data(), q.data.size());
+    const float* dk = alias ? dq : gpu::upload_async(t_buf.k, k.data.data(), k.data.size());
+    float* dff = fflow ? gpu::upload_async(t_buf.ff, fflow->data.data(), fflow->data.size()) : nullptr;
+    float* dbf = fflow ? gpu::upload_async(t_buf.bf, bflow->data.data(), bflow->data.size()) : nullptr;
+    gpu::profile_mark("forward: upload enqueued");
     float* dsims = t_buf.sims.f32(n_sel);
     float* doffs = t_buf.offsets.f32(n_sel * 3);
-    float* dch = cs > 0 ? t_buf.chains.f32(n_sel * cs * 6) : nullptr;
     const snls_config c = gpu::to_abi(cfg);
     gpu::check(snls_search_fwd(ctx, &c, dims_of(q), dq, dk, dff, dbf,
                                policy.mode == SearchMode::kFullGrid ? SNLS_MODE_FULLGRID
                                                                     : SNLS_MODE_FUSED,
-                               dsims, doffs, dch, nullptr));
+                               dsims, doffs, nullptr, nullptr));
+    // the whole result in the reference's fp64 layout, on the device: sims, offsets and the
+    // exact fp64 tape (centres, absolute chain links; snls_search_results64)
+    double* s64 = static_cast<double*>(t_buf.sims64.reserve(n_sel * sizeof(double)));
+    double* o64 = static_cast<double*>(t_buf.offs64.reserve(n_sel * 3 * sizeof(double)));
+    double* c64 = static_cast<double*>(t_buf.cen64.reserve(n_sel * 3 * sizeof(double)));
+    double* ch64 = cs > 0 ? static_cast<double*>(t_buf.ch64.reserve(n_sel * cs * 6 * sizeof(double))) : nullptr;
+    gpu::check(snls_search_results64(ctx, &c, dims_of(q), 0, q.t, dff, dbf, dsims, doffs, s64, o64, c64, ch64));
+    gpu::profile_mark("forward: kernels enqueued");
     gpu::check(snls_ctx_sync_check(ctx));
-    gpu::download(res.sims.values, dsims, n_sel);
-    gpu::download(res.offsets.data, doffs, n_sel * 3);
-    res.tape.centers.resize(n_sel * 3);
-    res.tape.chains.resize(n_sel * cs * 6);
-    // device chains (relative to the query pixel) stay in the pinned staging buffer and are
-    // converted to the reference's absolute positions in one parallel pass
-    const float* rel = nullptr;
-    if (cs > 0) {
-        float* st = gpu::staging(n_sel * cs * 6);
-        gpu::check(snls_copy_d2h(ctx, st, dch, n_sel * cs * 6 * sizeof(float)));
-        rel = st;
-    }
-    double* centers = res.tape.centers.data();
-    double* chains = res.tape.chains.data();
-    const double* offs = res.offsets.data.data();
-#pragma omp parallel for schedule(static) num_threads(policy.resolved_threads())
-    for (std::int64_t row = 0; row < rows; ++row) {
-        double qt, qy, qx;
-        query_base(grid, row, qt, qy, qx);
-        for (int li = 0; li < L; ++li) {
-            const std::size_t e = std::size_t(row) * L + li;
-            const double* o = offs + e * 3;
-            centers[e * 3 + 0] = qt + o[0];
-            centers[e * 3 + 1] = qy + o[1];
-            centers[e * 3 + 2] = qx + o[2];
-            const int links = std::max(int(std::lround(std::abs(o[0]))) - 1, 0);
-            for (int kk = 0; kk < cs; ++kk) {  // relative -> absolute positions (unused: 0)
-                const std::size_t b = (e * cs + kk) * 6;
-                if (kk < links) {
-                    chains[b + 0] = qy + double(rel[b + 0]);
-                    chains[b + 1] = qx + double(rel[b + 1]);
-                    for (int j = 2; j < 6; ++j) chains[b + j] = double(rel[b + j]);
-                } else {
-                    for (int j = 0; j < 6; ++j) chains[b + j] = 0.0;
-                }
-            }
-        }
-    }
+    gpu::profile_mark("forward: device done");
+    if (big) prep[1].join();  // the small vectors first: their copies overlap the chains' zero-fill
+    else prep_small();
+    gpu::profile_mark("forward: small vectors sized");
+    gpu::download64(res.sims.values, s64, n_sel);
+    gpu::download64(res.offsets.data, o64, n_sel * 3);
+    gpu::download64(res.tape.centers, c64, n_sel * 3);
+    if (big) prep[0].join();
+    else prep_chains();
+    gpu::profile_mark("forward: chains sized");
+    if (cs > 0) gpu::download64(res.tape.chains, ch64, n_sel * cs * 6);
+    gpu::profile_mark("forward: results downloaded");
     return res;
+}
+}  // namespace
+
+SearchResult shifted_nls_forward(const VideoTensor& q, const VideoTensor& k,
+                                 const FlowField& fflow, const FlowField& bflow,
+                                 const SearchConfig& cfg, const ExecPolicy& policy) {
+    return forward_impl(q, k, &fflow, &bflow, cfg, policy);
 }
 
 SearchResult nls_forward(const VideoTensor& q, const VideoTensor& k, const SearchConfig& cfg,
                          const ExecPolicy& policy) {
-    const FlowField zero_f(q.t, q.h, q.w, FlowDirection::kForward);
-    const FlowField zero_b(q.t, q.h, q.w, FlowDirection::kBackward);
-    return shifted_nls_forward(q, k, zero_f, zero_b, cfg, policy);
+    return forward_impl(q, k, nullptr, nullptr, cfg, policy);  // zero flows: NULL at the C-ABI
 }
 
 std::pair<SimilarityTensor, OffsetTensor> top_l(const SimilarityTensor& full,
@@ -302,35 +311,50 @@ void tape_to_device(const SearchTape& tape, float*& doffs, float*& dch) {
 SearchGradients shifted_nls_backward(const SimilarityTensor& grad_selected,
                                      const SearchTape& tape, const VideoTensor& q,
                                      const VideoTensor& k, const ExecPolicy& policy) {
-    (void)policy;  // device backward is the atomic form in either mode
     if (grad_selected.rows != tape.grid.rows() || grad_selected.cols != tape.cfg.topl)
         throw DomainError("shifted_nls_backward: gradient shape does not match the tape");
     if (q.t != tape.vid_t || q.h != tape.vid_h || q.w != tape.vid_w || q.f != tape.vid_f ||
         !q.same_shape(k))
         throw DomainError("shifted_nls_backward: tensor shape does not match the tape");
     SearchGradients g;
-    g.grad_q = VideoTensor(q.t, q.h, q.w, q.f);
-    g.grad_k = VideoTensor(q.t, q.h, q.w, q.f);
-    g.grad_fflow = FlowField(q.t, q.h, q.w, FlowDirection::kForward);
-    g.grad_bflow = FlowField(q.t, q.h, q.w, FlowDirection::kBackward);
     snls_ctx* ctx = gpu::context();
-    float *doffs = nullptr, *dch = nullptr;
-    tape_to_device(tape, doffs, dch);
-    float* dgrad = gpu::upload(t_buf.grad, grad_selected.values);
-    float* dq = gpu::upload(t_buf.q, q.data);
-    float* dk = gpu::upload(t_buf.k, k.data);
-    const std::uint64_t nv = q.size(), nf = g.grad_fflow.data.size();
+    gpu::profile_mark("backward: checks");
+    // the reference's own fp64 tape goes to the device as is (snls_search_bwd_ex): exact key
+    // centres and chain links, no host conversion
+    const std::uint64_t n_sel = std::uint64_t(tape.grid.rows()) * tape.cfg.topl;
+    const int cs = tape.chain_stride;
+    double* dcen = static_cast<double*>(t_buf.cen64.reserve(n_sel * 3 * sizeof(double)));
+    gpu::check(snls_copy_h2d(ctx, dcen, tape.centers.data(), n_sel * 3 * sizeof(double)));
+    double* dch = nullptr;
+    if (tape.cfg.wt > 1) {
+        dch = static_cast<double*>(t_buf.ch64.reserve(n_sel * std::max(cs, 1) * 6 * sizeof(double)));
+        gpu::check(snls_copy_h2d(ctx, dch, tape.chains.data(), n_sel * cs * 6 * sizeof(double)));
+    }
+    float* dgrad = gpu::upload_async(t_buf.grad, grad_selected.values.data(), grad_selected.values.size());
+    float* dq = gpu::upload_async(t_buf.q, q.data.data(), q.data.size());
+    const bool alias = (&q == &k || q.data == k.data);
+    float* dk = alias ? dq : gpu::upload_async(t_buf.k, k.data.data(), k.data.size());
+    const std::uint64_t nv = q.size(), nf = std::uint64_t(q.t) * q.h * q.w * 2;
     float* ddq = t_buf.dq.f32(nv);
     float* ddk = t_buf.dk.f32(nv);
     float* ddff = t_buf.dff.f32(nf);
     float* ddbf = t_buf.dbf.f32(nf);
     const snls_config c = gpu::to_abi(tape.cfg);
-    gpu::check(snls_search_bwd(ctx, &c, dims_of(q), dgrad, doffs, dch, dq, dk, ddq, ddk, ddff, ddbf));
+    // ExecPolicy::deterministic (the reference's default, search.cpp:687-696): bitwise
+    // reproducible fixed-point accumulation on the device
+    gpu::check(snls_search_bwd_ex(ctx, &c, dims_of(q), 0, q.t, dgrad, nullptr, nullptr, dcen, dch, dq, dk,
+                                  ddq, ddk, ddff, ddbf, policy.deterministic ? SNLS_BWD_DETERMINISTIC : 0));
     gpu::check(snls_ctx_sync_check(ctx));
+    gpu::profile_mark("backward: device done");
+    g.grad_q = VideoTensor(q.t, q.h, q.w, q.f);
+    g.grad_k = VideoTensor(q.t, q.h, q.w, q.f);
+    g.grad_fflow = FlowField(q.t, q.h, q.w, FlowDirection::kForward);
+    g.grad_bflow = FlowField(q.t, q.h, q.w, FlowDirection::kBackward);
     gpu::download(g.grad_q.data, ddq, nv);
     gpu::download(g.grad_k.data, ddk, nv);
     gpu::download(g.grad_fflow.data, ddff, nf);
     gpu::download(g.grad_bflow.data, ddbf, nf);
+    gpu::profile_mark("backward: downloaded");
     return g;
 }
 

@@ -312,7 +312,8 @@ def run_ours(args, wl):
         if train:  # backward: wpsum_backward (dV, dW) then shifted_nls_backward (dQ, dK, dFlow)
             ev_bwd.record(stream)
             S.wpsum_backward(g_out, counts, vid, wts, offs, cfg, ctx=ctx, check=False)
-            S.shifted_nls_backward(g_sims, res, vid, vid, ctx=ctx, check=False)
+            S.shifted_nls_backward(g_sims, res, vid, vid, ctx=ctx, check=False,
+                                   deterministic=args.deterministic)
 
     # correctness gate before timing: device error latch must be clean
     ev_mid = torch.cuda.Event(enable_timing=True)
@@ -402,7 +403,8 @@ def run_ours(args, wl):
             S.wpsum(v2, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
             if train:
                 S.wpsum_backward(g_out, counts, v2, wts, offs, cfg, ctx=ctx, check=False)
-                S.shifted_nls_backward(g_sims, res, v2, v2, ctx=ctx, check=False)
+                S.shifted_nls_backward(g_sims, res, v2, v2, ctx=ctx, check=False,
+                                       deterministic=args.deterministic)
             sims_p.copy_(sims, non_blocking=True)
             offs_p.copy_(offs, non_blocking=True)
             out_p.copy_(out, non_blocking=True)
@@ -680,6 +682,8 @@ def main():
                     choices=["auto", "tiled", "stream"], help="stride1 == 1 register plan")
     ap.add_argument("--videos-per-gpu", type=int, default=1,
                     help="independent videos per rank and step (c4/c2; SURVEY 8e scaling ratio)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="c3: the backward in the reference's deterministic mode (int64 fixed point)")
     ap.add_argument("--mock-cpu", action="store_true",
                     help="plumbing check without a GPU: gloo ranks, a numpy stand-in step, same "
                          "launch / barrier / max-over-ranks / JSON path (tests/test_bench.py)")

@@ -387,6 +387,9 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 #ifndef SNLS_WQ_FRAMES
 #define SNLS_WQ_FRAMES 0
 #endif
+#ifndef SNLS_WQ_MINB
+#define SNLS_WQ_MINB 2
+#endif
 // A CTA owns a TY x TX output tile of one frame (all channels).  Phase A: every query whose
 // write set (footprint + stride-cell remainder, aggregate.cpp:80-100) can meet the tile is
 // handled by one group of G lanes (float4 of channels each); for each neighbour l it reads the
@@ -400,7 +403,7 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 // videos (F = 64) split their channels over two CTAs and keep the parked patches, and the
 // shared memory per CTA, at the F = 32 size (two resident CTAs per SM instead of one).
 template <int P, int G, int FG, int TY, int TX>
-__global__ void __launch_bounds__(256, 2) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
+__global__ void __launch_bounds__(256, SNLS_WQ_MINB) wpsum_query_kernel(AggArgs a, float* __restrict__ out,
                                                           int32_t* __restrict__ counts) {
     extern __shared__ float4 s_patch[];  // [query][P*P][G]
     constexpr int HP = P / 2, NQG = 256 / G;

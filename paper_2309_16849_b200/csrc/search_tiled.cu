@@ -117,6 +117,15 @@ constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
 #define SNLS_ASSIGN1 1
 #endif
 constexpr bool kAssign1 = SNLS_ASSIGN1 != 0;
+// cp.async staging of the raw K rows (north star: "stages each block's shifted search-window
+// tile into shared memory via TMA or cp.async"): per lane a 3-row ring in shared memory, raw
+// row r+2 copied (LDGSTS) while region row r is interpolated from rows r, r+1.  A/B only
+// (profiles/r01_plans.txt): the ring costs 86 KB of shared memory per CTA at c4 (2 CTAs/SM
+// instead of 4)
+#ifndef SNLS_CPASYNC
+#define SNLS_CPASYNC 0
+#endif
+constexpr bool kCpAsync = SNLS_CPASYNC != 0;
 #ifndef SNLS_BSPLIT
 #define SNLS_BSPLIT 2
 #endif
@@ -248,6 +257,23 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             for (int b = 0; b < W; ++b) acc[s][b] = 0.f;
 
         const uint32_t slot_base = uint32_t(fp) * W * W;
+        // kCpAsync: ring[slot][j][thread] after the query patch in dynamic shared memory
+        [[maybe_unused]] float4* ring = reinterpret_cast<float4*>(s_qdyn) + size_t(C::QPB) * P * P * G;
+        [[maybe_unused]] auto issue_row = [&](int raw, int slot) {
+            const float4* kb4 = reinterpret_cast<const float4*>(kframe);
+            const unsigned rr = unsigned(reflect_near(by + raw, H)) * rowv;
+#pragma unroll
+            for (int j = 0; j <= R; ++j)
+                cp_async16(ring + (size_t(slot) * (R + 1) + j) * 128 + threadIdx.x,
+                           kb4 + (rr + (interior ? xb + unsigned(j) * G : xo[j * XS])));
+        };
+        if constexpr (kPackedPath && kCpAsync) {
+            issue_row(0, 0);
+            cp_async_commit();
+            issue_row(1, 1);
+            cp_async_commit();
+        }
+        int rs0 = 0;  // ring slot of raw row r
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
@@ -261,7 +287,23 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                 const float4* kb4 = reinterpret_cast<const float4*>(kframe);
                 const u64 W00 = pk2(w00, w00), W01 = pk2(w01, w01), W10 = pk2(w10, w10), W11 = pk2(w11, w11);
                 P4 kr[R];
-                if (interior) {
+                if constexpr (kCpAsync) {
+                    const int rs1 = rs0 == 2 ? 0 : rs0 + 1, rs2 = rs1 == 2 ? 0 : rs1 + 1;
+                    if (r + 2 <= R) issue_row(r + 2, rs2);
+                    cp_async_commit();
+                    cp_async_wait<1>();  // raw rows r and r+1 have landed (own lane's copies)
+                    const float4* q0 = ring + size_t(rs0) * (R + 1) * 128 + threadIdx.x;
+                    const float4* q1 = ring + size_t(rs1) * (R + 1) * 128 + threadIdx.x;
+                    P4 a0 = lds_p4(q0), a1 = lds_p4(q1);
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const P4 b0 = lds_p4(q0 + (j + 1) * 128), b1 = lds_p4(q1 + (j + 1) * 128);
+                        kr[j] = lerp2(a0, b0, a1, b1, W00, W01, W10, W11);
+                        a0 = b0;
+                        a1 = b1;
+                    }
+                    rs0 = rs1;
+                } else if (interior) {
                     const float4* p0 = kb4 + (r0 + xb);
                     const float4* p1 = kb4 + (r1 + xb);
                     P4 a0 = ldp4(p0), a1 = ldp4(p1);
@@ -526,7 +568,8 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     constexpr bool QSM = kQsm && VEC == 2;
     constexpr bool QREG = P >= 7 && !QSM;
     const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64)
-                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
+                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0) +
+                                  (VEC == 4 && kPacked && kCpAsync ? size_t(3) * (C::R + 1) * 128 * sizeof(float4) : 0);
     auto launch = [&](auto kern) {
         ensure_smem(kern, smem);
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);

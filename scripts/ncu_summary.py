@@ -11,7 +11,10 @@ KEYS = ["gpu__time_duration.sum", "launch__registers_per_thread", "sm__warps_act
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
         "lts__t_sector_hit_rate.pct", "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size"]
+        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "launch__occupancy_limit_registers",
+        "launch__occupancy_limit_shared_mem", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 def main(rep):
     hdr, units, rows = raw(rep)

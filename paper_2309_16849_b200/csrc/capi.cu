@@ -1,6 +1,8 @@
 // The C-ABI (include/snls_cuda.h): validation with the reference's messages, dispatch to
 // the sm_100a kernels, and the per-(device, stream) context.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <initializer_list>
@@ -129,6 +131,26 @@ bool underfull(const snls_config* c, int t, int t0 = 0, int t1 = -1) {
         if (worst < 0 || valid < worst) worst = valid;
     }
     return worst < c->topl;
+}
+
+// Temporally blocked raster for the tiled search (common.cuh band_row): only when the key
+// frames one query frame reads overflow about a third of the 126 MB L2; band height such
+// that (2wt+2) frames of band rows (plus the window reach) fit that budget.
+// SNLS_SEARCH_BAND overrides (0 = plain raster).
+int search_band(const snls_config* c, snls_dims d) {
+    static const int env = [] {
+        const char* e = std::getenv("SNLS_SEARCH_BAND");
+        return e ? std::atoi(e) : -1;
+    }();
+    const int nh = (d.h - 1) / c->stride0 + 1;
+    if (env >= 0) return env >= nh ? 0 : env;
+    const double row_bytes = double(d.w) * d.f * 4.0;
+    const double frames_bytes = (2.0 * c->wt + 1) * d.h * row_bytes;
+    const double budget = 42.0e6;
+    if (frames_bytes <= budget) return 0;
+    const double px_rows = budget / ((2.0 * c->wt + 2) * row_bytes) - 2.0 * (c->ws / 2 + c->ps / 2 + 4);
+    const int band = std::max(4, int(px_rows / c->stride0));
+    return band >= nh ? 0 : band;
 }
 
 int ensure_work(snls_ctx* ctx, size_t bytes) {
@@ -446,7 +468,8 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
         int produced = 0;
         if (!ctx->force_generic && cfg->stride1 == 1.0) {
             TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
-                           sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid, ctx->search_kernel};
+                           sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid, ctx->search_kernel,
+                           search_band(cfg, dims)};
             produced = launch_search_tiled(ts, ctx->stream, nullptr);
             if (produced < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
         }
@@ -470,7 +493,8 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
     int tiled = 0, used = 0;
     if (!ctx->force_generic && cfg->stride1 == 1.0) {
         TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
-                       sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr, ctx->search_kernel};
+                       sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr, ctx->search_kernel,
+                       search_band(cfg, dims)};
         tiled = launch_search_tiled(ts, ctx->stream, &used);
         if (tiled < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
     }

@@ -93,6 +93,24 @@ __device__ __forceinline__ void row_coords(const Dims& d, int64_t local_row, int
     qt = int(r / d.nh);
 }
 
+// Temporally blocked raster: CTA-order index p -> query row (local to the frame range).  The
+// rows are enumerated band by band (`band` query rows of every frame), and inside a band
+// frame by frame, then (y, x): consecutive CTAs work on one band of consecutive frames, so
+// the key frames a band reads (qt - wt .. qt + wt) stay in L2 across the 2wt+1 query frames
+// that reuse them, instead of the whole frame set being streamed from HBM once per query
+// frame when it exceeds the L2 (c5: 5 frames x 67 MB).
+__device__ __forceinline__ int64_t band_row(const Dims& d, int64_t p, int band) {
+    const int64_t full = int64_t(band) * d.nw * d.nt;  // rows of one complete band (all frames)
+    const int64_t b = p / full;
+    const int64_t q = p - b * full;
+    const int y0 = int(b) * band;
+    const int hb = min(band, d.nh - y0);
+    const int64_t per_frame = int64_t(hb) * d.nw;
+    const int64_t t = q / per_frame;
+    const int64_t rem = q - t * per_frame;
+    return (t * d.nh + y0 + rem / d.nw) * d.nw + rem % d.nw;
+}
+
 // search.cpp:59-68: frame scan order 0, -1, +1, -2, +2, ...
 __host__ __device__ __forceinline__ int scan_dt(int fpos) {
     return fpos == 0 ? 0 : ((fpos & 1) ? -((fpos + 1) / 2) : fpos / 2);

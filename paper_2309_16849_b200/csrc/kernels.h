@@ -35,6 +35,8 @@ struct TiledSearch {
     int num_sms;
     float* grid;  // kFullGrid: write every window score (rows x slots) and skip selection
     int kernel;   // register plan: 0 auto, 1 region-row tiled, 2 streaming
+    int band = 0;  // > 0: temporally blocked raster, bands of `band` query rows swept frame by
+                   // frame (search_tiled.cu, band_row); 0: plain (t, y, x) raster
 };
 
 struct AggArgs {

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     const int qslot = warp * C::QPW + gq;
     const int64_t row_raw = int64_t(blockIdx.x) * C::QPB + qslot;
     const bool row_ok = row_raw < a.d.rows;
-    const int64_t row = row_ok ? row_raw : a.d.rows - 1;
+    const int64_t row = row_ok ? (a.band > 0 ? band_row(a.d, row_raw, a.band) : row_raw) : a.d.rows - 1;
     int qt, qy, qx;
     row_coords(a.d, row, qt, qy, qx);
     const int H = a.d.h, Wd = a.d.w;

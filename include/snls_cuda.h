@@ -96,6 +96,10 @@ int snls_ctx_force_generic(snls_ctx* ctx, int on);
  * 2 query-stationary streaming (ps in {3, 7}, F in {32, 64}; else tiled).  Results agree to the parity tolerance; each plan is
  * deterministic and tie-exact on its own. */
 int snls_ctx_set_search_kernel(snls_ctx* ctx, int kind);
+/* Raster of the tiled search: -1 auto (temporally blocked in bands of query rows when the
+ * key frames a query frame reads overflow ~1/3 of L2, e.g. c5), 0 plain (t, y, x), > 0 that
+ * many query rows per band.  Results are identical either way (each query is independent). */
+int snls_ctx_set_search_band(snls_ctx* ctx, int band);
 
 /* ---- device memory through the context (so C++ callers need no CUDA headers) --------- */
 int snls_device_alloc(snls_ctx* ctx, uint64_t bytes, void** out);
@@ -143,9 +147,17 @@ int snls_search_grid(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, cons
 int snls_topl(snls_ctx* ctx, int64_t rows, int cols, const float* full,
               const float* full_offsets, int topl, float* sel, float* sel_offsets);
 
-/* Replaces snls::replay_similarities (search.hpp:157-158; search.cpp:470-493). */
+/* Replaces snls::replay_similarities (search.hpp:157-158; search.cpp:470-493) from the fp32
+ * device tape: the generic per-slot arithmetic at query + offset (agrees with the forward to
+ * the fp32 tolerance). */
 int snls_replay(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* q,
                 const float* k, const float* offsets, float* sims);
+/* replay_similarities from the fp64 tape (centres, snls_search_tape64 / the reference's
+ * SearchTape) through a search plan's OWN per-slot arithmetic -- bitwise equal to that plan's
+ * forward (search.cpp:470-493, test_search.cpp:539-553): plan 0 generic, 1 region-row tiled,
+ * 2 streaming, -1 the plan snls_search_fwd takes for this configuration and context. */
+int snls_replay64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                  const float* q, const float* k, const double* centers, int plan, float* sims);
 
 /* Replaces snls::shifted_nls_backward (search.hpp:151-153; search.cpp:671-711).
  * Gradients are accumulated with atomics (the reference's non-deterministic mode); the

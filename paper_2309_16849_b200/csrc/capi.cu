@@ -25,6 +25,7 @@ struct snls_ctx {
     int force_generic = 0;
     int search_kernel = 0;
     int last_path = -1;
+    int band = -1;  // temporally blocked search raster: -1 auto (search_band), 0 off, > 0 rows
 };
 
 namespace snls_capi {
@@ -137,13 +138,14 @@ bool underfull(const snls_config* c, int t, int t0 = 0, int t1 = -1) {
 // frames one query frame reads overflow about a third of the 126 MB L2; band height such
 // that (2wt+2) frames of band rows (plus the window reach) fit that budget.
 // SNLS_SEARCH_BAND overrides (0 = plain raster).
-int search_band(const snls_config* c, snls_dims d) {
+int search_band(const snls_ctx* ctx, const snls_config* c, snls_dims d) {
     static const int env = [] {
         const char* e = std::getenv("SNLS_SEARCH_BAND");
         return e ? std::atoi(e) : -1;
     }();
     const int nh = (d.h - 1) / c->stride0 + 1;
-    if (env >= 0) return env >= nh ? 0 : env;
+    const int forced = ctx->band >= 0 ? ctx->band : env;
+    if (forced >= 0) return forced >= nh ? 0 : forced;
     const double row_bytes = double(d.w) * d.f * 4.0;
     const double frames_bytes = (2.0 * c->wt + 1) * d.h * row_bytes;
     const double budget = 42.0e6;
@@ -286,6 +288,12 @@ int snls_ctx_set_search_kernel(snls_ctx* ctx, int kind) {
     if (int rc = check_ctx(ctx)) return rc;
     if (kind < 0 || kind > 2) return fail(SNLS_EARG, "set_search_kernel: kind must be 0, 1 or 2");
     ctx->search_kernel = kind;
+    return SNLS_OK;
+}
+
+int snls_ctx_set_search_band(snls_ctx* ctx, int band) {
+    if (int rc = check_ctx(ctx)) return rc;
+    ctx->band = band < 0 ? -1 : band;
     return SNLS_OK;
 }
 
@@ -469,7 +477,7 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
         if (!ctx->force_generic && cfg->stride1 == 1.0) {
             TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
                            sims, offsets, chains, weights, ctx->err, ctx->num_sms, grid, ctx->search_kernel,
-                           search_band(cfg, dims)};
+                           search_band(ctx, cfg, dims)};
             produced = launch_search_tiled(ts, ctx->stream, nullptr);
             if (produced < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
         }
@@ -494,7 +502,7 @@ int snls_search_fwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims
     if (!ctx->force_generic && cfg->stride1 == 1.0) {
         TiledSearch ts{q, k, ff, bf, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, beta,
                        sims, offsets, chains, weights, ctx->err, ctx->num_sms, nullptr, ctx->search_kernel,
-                       search_band(cfg, dims)};
+                       search_band(ctx, cfg, dims)};
         tiled = launch_search_tiled(ts, ctx->stream, &used);
         if (tiled < 0) return fail(SNLS_ECUDA, "search: tiled kernel launch failed");
     }
@@ -552,6 +560,39 @@ int snls_replay(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const flo
     const Dims d = make_dims(dims, cfg->stride0);
     return after_launch(ctx, launch_replay(q, k, d, cfg->ps, cfg->metric, cfg->topl, offsets, sims, ctx->stream),
                         "snls_replay");
+}
+
+int snls_replay64(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                  const float* q, const float* k, const double* centers, int plan, float* sims) {
+    if (int rc = check_ctx(ctx)) return rc;
+    if (int rc = validate(cfg)) return rc;
+    if (int rc = check_dims(dims)) return rc;
+    if (!q || !k || !centers || !sims) return fail(SNLS_EARG, "replay_similarities: null tensor");
+    if (int rc = check_aligned("replay_similarities", {q, k})) return rc;
+    if (t0 < 0 || t1 > dims.t || t0 >= t1) return fail(SNLS_EARG, "replay_similarities: empty or invalid frame range");
+    if (plan < -1 || plan > 2) return fail(SNLS_EARG, "replay_similarities: plan must be -1, 0, 1 or 2");
+    DeviceGuard g(ctx->device);
+    const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
+    if (plan == -1)  // the plan the forward takes for this configuration (snls_search_fwd)
+        plan = (!ctx->force_generic && cfg->stride1 == 1.0) ? (ctx->search_kernel == 2 ? 2 : 1) : 0;
+    TiledSearch ts{q, k, nullptr, nullptr, d, cfg->ws, cfg->wt, cfg->ps, cfg->topl, cfg->metric, 1.f,
+                   nullptr, nullptr, nullptr, nullptr, ctx->err, ctx->num_sms, sims, ctx->search_kernel};
+    ts.tape = centers;
+    ts.d.rows = d.rows * cfg->topl;  // one replay "row" per selected entry
+    int n = 0;
+    if (plan == 2) {
+        if (int rc = ensure_work(ctx, size_t(ts.d.rows) * cfg->ps * cfg->ps * sizeof(float))) return rc;
+        ts.grid = static_cast<float*>(ctx->work);
+        n = launch_replay_stream(ts, sims, ctx->stream);
+        if (n == 0) plan = 1;  // not instantiated for this shape: the forward took the tiled plan
+        ts.grid = sims;
+    }
+    if (plan == 1 && n == 0) {
+        n = launch_replay_tiled(ts, ctx->stream);
+        if (n == 0) plan = 0;  // the forward took the generic plan
+    }
+    if (plan == 0 && n == 0) n = launch_replay64(q, k, d, cfg->ps, cfg->metric, cfg->topl, centers, sims, ctx->stream);
+    return after_launch(ctx, n, "snls_replay64");
 }
 
 int snls_search_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad,

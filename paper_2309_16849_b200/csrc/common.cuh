@@ -171,6 +171,22 @@ __device__ __forceinline__ float blend(const Taps& t, float a, float b, float c,
     return t.w00 * a + t.w01 * b + t.w10 * c + t.w11 * d;
 }
 
+#ifndef SNLS_SHIFT_GRID
+#define SNLS_SHIFT_GRID 2
+#endif
+// A shift rounded to the 2^-32 grid (two adds: the ulp of 1.5 * 2^20 is 2^-32; |v| < 2^19,
+// beyond that a coarser grid, which keeps the same exactness property).
+__device__ __forceinline__ double grid32(double v) {
+#if SNLS_SHIFT_GRID == 2
+    constexpr double kMagic = 0x1.8p20;
+    return (v + kMagic) - kMagic;
+#elif SNLS_SHIFT_GRID == 1
+    return rint(v * 0x1p32) * 0x1p-32;
+#else
+    return v;
+#endif
+}
+
 // search.cpp:72-122 on device: the window shift to frame qt + dt in fp64.  dt == 0 reads
 // the forward field at the query pixel; |dt| >= 1 sums per-step fields, later links
 // bilinear-sampled at the displaced position.  `links` (optional) receives |dt|-1 links of
@@ -194,8 +210,8 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
         return double(__ldg(fl + ((size_t(t) * h + y) * w + x) * 2 + c));
     };
     if (dt == 0) {
-        dy = at(ff, qt, qy, qx, 0);
-        dx = at(ff, qt, qy, qx, 1);
+        dy = grid32(at(ff, qt, qy, qx, 0));  // (2^-32 grid: see the end)
+        dx = grid32(at(ff, qt, qy, qx, 1));
         return;
     }
     const float* fld = dt > 0 ? ff : bf;
@@ -212,7 +228,10 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
             const double py = double(qy) + sy, px = double(qx) + sx;
             const double fby = floor(py), fbx = floor(px);
             const double fy = py - fby, fx = px - fbx;
-            const int iby = int_base(fby), ibx = int_base(fbx);
+#ifndef SNLS_LINK_CLAMP
+#define SNLS_LINK_CLAMP 1
+#endif
+            const int iby = SNLS_LINK_CLAMP ? int_base(fby) : int(fby), ibx = SNLS_LINK_CLAMP ? int_base(fbx) : int(fbx);
             const int y0 = reflect_near(iby, h), y1 = reflect_near(iby + 1, h);
             const int x0 = reflect_near(ibx, w), x1 = reflect_near(ibx + 1, w);
             const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);
@@ -236,13 +255,16 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
         sy += vy;
         sx += vx;
     }
-    dy = sy;
-    dx = sx;
+    // the shift on a 2^-32 grid (|change| < 2^-33 px, far below fp32's fraction): the key
+    // centres (qy + sdy) + n of the fp64 tape are then exact, so a replay from a centre sees
+    // the very fraction the forward interpolated with (replay_similarities == forward, bitwise)
+    dy = grid32(sy);
+    dx = grid32(sx);
 }
 
-__device__ __forceinline__ void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
-                                         int h, int w, int qt, int qy, int qx, int dt, double& dy,
-                                         double& dx, float* links) {
+__device__ inline void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
+                                int h, int w, int qt, int qy, int qx, int dt, double& dy,
+                                double& dx, float* links) {
     shift_to_t<float>(ff, bf, h, w, qt, qy, qx, dt, dy, dx, links);
 }
 

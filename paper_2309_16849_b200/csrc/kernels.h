@@ -37,6 +37,7 @@ struct TiledSearch {
     int kernel;   // register plan: 0 auto, 1 region-row tiled, 2 streaming
     int band = 0;  // > 0: temporally blocked raster, bands of `band` query rows swept frame by
                    // frame (search_tiled.cu, band_row); 0: plain (t, y, x) raster
+    const double* tape = nullptr;  // replay: fp64 centres (kt, ky, kx) per entry (rows = entries)
 };
 
 struct AggArgs {
@@ -57,6 +58,12 @@ int launch_search_generic(const GenericSearch& g, cudaStream_t st);
 int launch_search_tiled(const TiledSearch& s, cudaStream_t st, int* used);
 // Query-stationary streaming variant (search_stream.cu); 0 when not instantiated.
 int launch_search_stream(const TiledSearch& s, cudaStream_t st);
+// replay_similarities through the tiled plan's own arithmetic (bitwise equal to its forward):
+// s.tape = centres, s.grid = the rows x topl output, s.d = the query dims; 0 if not instantiated
+int launch_replay_tiled(const TiledSearch& s, cudaStream_t st);
+int launch_replay_stream(const TiledSearch& s, float* out, cudaStream_t st);
+int launch_replay64(const float* q, const float* k, Dims d, int ps, int metric, int topl,
+                    const double* centers, float* sims, cudaStream_t st);
 int launch_topl(int64_t rows, int cols, const float* full, const float* full_offsets, int topl,
                 float* sel, float* sel_offsets, int* err, cudaStream_t st);
 int launch_emit_tape(const float* ff, const float* bf, Dims d, int wt, int topl,

@@ -43,17 +43,4 @@ __device__ __forceinline__ P4 ldp4(const float4* p) {
     return {pk2(v.x, v.y), pk2(v.z, v.w)};
 }
 
-// 16-byte asynchronous global -> shared copy (LDGSTS), cached in L1 (.ca), and its groups
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ P4 lds_p4(const float4* p) {
-    const float4 v = *p;
-    return {pk2(v.x, v.y), pk2(v.z, v.w)};
-}
-
 }  // namespace snls_gpu

@@ -424,6 +424,31 @@ int launch_tape64(const float* ff, const float* bf, Dims d, int ws, int wt, int 
     return 1;
 }
 
+// replay through the generic plan at the fp64 tape centres: the forward's own expression
+// for every slot (ky = (qy + sdy) + stride1 (dyi - ws/2), search_generic_kernel), so equal bits
+template <int VEC>
+__global__ void replay64_kernel(const float* q, const float* k, Dims d, int ps, int metric, int topl,
+                                const double* centers, float* sims) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= d.rows * topl) return;
+    int qt, qy, qx;
+    row_coords(d, e / topl, qt, qy, qx);
+    const double* c = centers + size_t(e) * 3;
+    const int kt = int(c[0]);
+    sims[e] = (kt >= 0 && kt < d.t) ? patch_sim_generic<VEC>(q, k, d, qt, qy, qx, kt, c[1], c[2], ps, metric)
+                                    : -INFINITY;
+}
+
+int launch_replay64(const float* q, const float* k, Dims d, int ps, int metric, int topl,
+                    const double* centers, float* sims, cudaStream_t st) {
+    const int64_t n = d.rows * topl;
+    if (d.f % 4 == 0)
+        replay64_kernel<4><<<unsigned((n + 127) / 128), 128, 0, st>>>(q, k, d, ps, metric, topl, centers, sims);
+    else
+        replay64_kernel<1><<<unsigned((n + 127) / 128), 128, 0, st>>>(q, k, d, ps, metric, topl, centers, sims);
+    return 1;
+}
+
 int launch_replay(const float* q, const float* k, Dims d, int ps, int metric, int topl,
                   const float* offsets, float* sims, cudaStream_t st) {
     const int64_t n = d.rows * topl;

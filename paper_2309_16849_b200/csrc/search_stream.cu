@@ -38,7 +38,11 @@ struct StreamCfg {
     static constexpr int QPW = 32 / G, WARPS = 4, QPB = QPW * WARPS;
 };
 
-template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB>
+// RP (replay_similarities, W = P): every "row" is one selected entry (row / topl its query),
+// frame and window centre from the entry's fp64 tape centre; the full-grid write of the
+// P x P window goes to a scratch row whose centre slot is the entry (the per-slot arithmetic
+// does not depend on the slot's place in the window: bitwise equal to the forward).
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool RP = false>
 __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a) {
     static_assert(W >= P, "window narrower than the patch: not instantiated");
     using C = StreamCfg<P, W, VEC, G>;
@@ -52,12 +56,12 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
     const bool row_ok = row_raw < a.d.rows;
     const int64_t row = row_ok ? row_raw : a.d.rows - 1;
     int qt, qy, qx;
-    row_coords(a.d, row, qt, qy, qx);
+    row_coords(a.d, RP ? row / a.topl : row, qt, qy, qx);
     const int H = a.d.h, Wd = a.d.w;
     const unsigned rowF = unsigned(Wd) * F;  // floats per image row
     const size_t frame_elems = size_t(H) * rowF;
     const int c0 = gl * VEC;
-    const int nfr = 2 * a.wt + 1;
+    const int nfr = RP ? 1 : 2 * a.wt + 1;
 
     // ---- the query patch, reflected integer pixels (search.cpp:129-132), in registers
     float qv[P][P][VEC];
@@ -77,15 +81,16 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
     float* grid_row = a.grid ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
-        const int dt = scan_dt(fp), kt = qt + dt;
+        const int dt = RP ? int(a.tape[size_t(row) * 3]) - qt : scan_dt(fp), kt = qt + dt;
         const bool on = row_ok && kt >= 0 && kt < a.d.t;
         if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
             if (a.grid && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
             continue;
         }
         double sdy = 0.0, sdx = 0.0;
-        if (on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
-        const double cy = double(qy) + sdy, cx = double(qx) + sdx;
+        if (!RP && on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
+        const double cy = RP ? a.tape[size_t(row) * 3 + 1] : double(qy) + sdy;
+        const double cx = RP ? a.tape[size_t(row) * 3 + 2] : double(qx) + sdx;
         const double fby = floor(cy), fbx = floor(cx);
         const float fy = float(cy - fby), fx = float(cx - fbx);
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
@@ -197,7 +202,41 @@ int launch_by_f(const TiledSearch& s, cudaStream_t st) {
     }
 }
 
+template <int P, int VEC, int G>
+int launch_replay_one(const TiledSearch& s, cudaStream_t st) {
+    using C = StreamCfg<P, P, VEC, G>;
+    const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
+    if (s.metric == SNLS_METRIC_IP)
+        search_stream_kernel<P, P, VEC, G, 16, SNLS_METRIC_IP, 1, true><<<blocks, 128, 0, st>>>(s);
+    else
+        search_stream_kernel<P, P, VEC, G, 16, SNLS_METRIC_L2, 1, true><<<blocks, 128, 0, st>>>(s);
+    return 1;
+}
+
+__global__ void centre_slot_kernel(const float* __restrict__ grid, int64_t n, int slots, int centre,
+                                   float* __restrict__ out) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < n) out[e] = grid[size_t(e) * slots + centre];
+}
+
 }  // namespace
+
+// replay through the streaming plan: s.tape = centres, s.grid = scratch of rows * ps^2 floats,
+// `out` = rows; 0 when the plan is not instantiated for this shape
+int launch_replay_stream(const TiledSearch& s, float* out, cudaStream_t st) {
+    if (s.topl > 16) return 0;
+    const bool inst = (s.ps == 7 && s.ws == 9) || (s.ps == 3 && (s.ws == 11 || s.ws == 9));
+    if (!inst) return 0;
+    int n = 0;
+    if (s.ps == 7) n = s.d.f == 64 ? launch_replay_one<7, 2, 32>(s, st) : 0;
+    else if (s.d.f == 32) n = launch_replay_one<3, 4, 8>(s, st);
+    else if (s.d.f == 64) n = launch_replay_one<3, 4, 16>(s, st);
+    if (!n) return 0;
+    const int P = s.ps;
+    centre_slot_kernel<<<unsigned((s.d.rows + 255) / 256), 256, 0, st>>>(s.grid, s.d.rows, P * P,
+                                                                         (P / 2) * P + P / 2, out);
+    return 2;
+}
 
 int launch_search_stream(const TiledSearch& s, cudaStream_t st) {
     if (s.topl > 16) return 0;

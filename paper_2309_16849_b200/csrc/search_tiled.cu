@@ -117,15 +117,6 @@ constexpr bool kXoSmem = SNLS_XO_SMEM != 0;
 #define SNLS_ASSIGN1 1
 #endif
 constexpr bool kAssign1 = SNLS_ASSIGN1 != 0;
-// cp.async staging of the raw K rows (north star: "stages each block's shifted search-window
-// tile into shared memory via TMA or cp.async"): per lane a 3-row ring in shared memory, raw
-// row r+2 copied (LDGSTS) while region row r is interpolated from rows r, r+1.  A/B only
-// (profiles/r01_plans.txt): the ring costs 86 KB of shared memory per CTA at c4 (2 CTAs/SM
-// instead of 4)
-#ifndef SNLS_CPASYNC
-#define SNLS_CPASYNC 0
-#endif
-constexpr bool kCpAsync = SNLS_CPASYNC != 0;
 #ifndef SNLS_BSPLIT
 #define SNLS_BSPLIT 2
 #endif
@@ -143,7 +134,15 @@ constexpr int kBSplitSmallW = SNLS_BSPLIT_SMALL_W;
 
 // FG: full-grid mode (materialise the scores; a separate instantiation so the fused kernel
 // carries no grid pointer or branches)
-template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG, bool FG>
+// RP (replay_similarities, W = 1): every "row" is one selected entry (row / topl is its
+// query), the single frame and window centre come from the entry's fp64 tape centre, and the
+// full-grid write stores its one slot: the same per-slot arithmetic as the forward (the
+// interpolation, the (py, px, pair) chains and the lane butterfly do not depend on the slot's
+// place in the window), so the replayed value equals the forward's bit for bit.
+// BAND: the temporally blocked raster (a separate instantiation: the remap's registers would
+// otherwise cost the plain-raster kernel a spill)
+template <int P, int W, int VEC, int G, int KMAX, int METRIC, int MINB, bool QREG, bool FG, bool RP = false,
+          bool BAND = false>
 __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) {
     using C = TiledCfg<P, W, VEC, G>;
     constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
@@ -160,13 +159,16 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     const int qslot = warp * C::QPW + gq;
     const int64_t row_raw = int64_t(blockIdx.x) * C::QPB + qslot;
     const bool row_ok = row_raw < a.d.rows;
-    const int64_t row = row_ok ? (a.band > 0 ? band_row(a.d, row_raw, a.band) : row_raw) : a.d.rows - 1;
+    // temporally blocked raster, remapped per CTA (its QPB queries stay consecutive in one image
+    // row when QPB divides nw): blockIdx-only arithmetic, kept in uniform registers
+    const int64_t row0 = BAND ? band_row(a.d, int64_t(blockIdx.x) * C::QPB, a.band) : int64_t(blockIdx.x) * C::QPB;
+    const int64_t row = row_ok ? row0 + qslot : a.d.rows - 1;
     int qt, qy, qx;
-    row_coords(a.d, row, qt, qy, qx);
+    row_coords(a.d, RP ? row / a.topl : row, qt, qy, qx);
     const int H = a.d.h, Wd = a.d.w;
     const size_t frame_elems = size_t(H) * Wd * F;
     const int c0 = gl * VEC;
-    const int nfr = 2 * a.wt + 1;
+    const int nfr = RP ? 1 : 2 * a.wt + 1;
 
     // query patch addressing (reflected, integer pixels; search.cpp:129-132)
     const float* qbase = a.q + size_t(qt) * frame_elems + c0;
@@ -210,15 +212,16 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     float* grid_row = FG ? a.grid + size_t(row) * nfr * W * W : nullptr;
 
     for (int fp = 0; fp < nfr; ++fp) {
-        const int dt = scan_dt(fp), kt = qt + dt;
+        const int dt = RP ? int(a.tape[size_t(row) * 3]) - qt : scan_dt(fp), kt = qt + dt;
         const bool on = row_ok && kt >= 0 && kt < a.d.t;
         if (!__any_sync(0xffffffffu, on)) {  // warp-uniform skip (search.cpp:300)
             if (FG && row_ok) write_off_frame<W, G>(a.grid, row, fp, nfr, gl);
             continue;
         }
         double sdy = 0.0, sdx = 0.0;
-        if (on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
-        const double cy = double(qy) + sdy, cx = double(qx) + sdx;
+        if (!RP && on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
+        const double cy = RP ? a.tape[size_t(row) * 3 + 1] : double(qy) + sdy;
+        const double cx = RP ? a.tape[size_t(row) * 3 + 2] : double(qx) + sdx;
         const double fby = floor(cy), fbx = floor(cx);
         const float fy = float(cy - fby), fx = float(cx - fbx);
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
@@ -257,23 +260,6 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
             for (int b = 0; b < W; ++b) acc[s][b] = 0.f;
 
         const uint32_t slot_base = uint32_t(fp) * W * W;
-        // kCpAsync: ring[slot][j][thread] after the query patch in dynamic shared memory
-        [[maybe_unused]] float4* ring = reinterpret_cast<float4*>(s_qdyn) + size_t(C::QPB) * P * P * G;
-        [[maybe_unused]] auto issue_row = [&](int raw, int slot) {
-            const float4* kb4 = reinterpret_cast<const float4*>(kframe);
-            const unsigned rr = unsigned(reflect_near(by + raw, H)) * rowv;
-#pragma unroll
-            for (int j = 0; j <= R; ++j)
-                cp_async16(ring + (size_t(slot) * (R + 1) + j) * 128 + threadIdx.x,
-                           kb4 + (rr + (interior ? xb + unsigned(j) * G : xo[j * XS])));
-        };
-        if constexpr (kPackedPath && kCpAsync) {
-            issue_row(0, 0);
-            cp_async_commit();
-            issue_row(1, 1);
-            cp_async_commit();
-        }
-        int rs0 = 0;  // ring slot of raw row r
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
             // ---- interpolate region row r (bilinear, 4 reflected taps; tensor.cpp:31-48)
@@ -287,23 +273,7 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
                 const float4* kb4 = reinterpret_cast<const float4*>(kframe);
                 const u64 W00 = pk2(w00, w00), W01 = pk2(w01, w01), W10 = pk2(w10, w10), W11 = pk2(w11, w11);
                 P4 kr[R];
-                if constexpr (kCpAsync) {
-                    const int rs1 = rs0 == 2 ? 0 : rs0 + 1, rs2 = rs1 == 2 ? 0 : rs1 + 1;
-                    if (r + 2 <= R) issue_row(r + 2, rs2);
-                    cp_async_commit();
-                    cp_async_wait<1>();  // raw rows r and r+1 have landed (own lane's copies)
-                    const float4* q0 = ring + size_t(rs0) * (R + 1) * 128 + threadIdx.x;
-                    const float4* q1 = ring + size_t(rs1) * (R + 1) * 128 + threadIdx.x;
-                    P4 a0 = lds_p4(q0), a1 = lds_p4(q1);
-#pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        const P4 b0 = lds_p4(q0 + (j + 1) * 128), b1 = lds_p4(q1 + (j + 1) * 128);
-                        kr[j] = lerp2(a0, b0, a1, b1, W00, W01, W10, W11);
-                        a0 = b0;
-                        a1 = b1;
-                    }
-                    rs0 = rs1;
-                } else if (interior) {
+                if (interior) {
                     const float4* p0 = kb4 + (r0 + xb);
                     const float4* p1 = kb4 + (r1 + xb);
                     P4 a0 = ldp4(p0), a1 = ldp4(p1);
@@ -568,12 +538,23 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
     constexpr bool QSM = kQsm && VEC == 2;
     constexpr bool QREG = P >= 7 && !QSM;
     const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64)
-                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0) +
-                                  (VEC == 4 && kPacked && kCpAsync ? size_t(3) * (C::R + 1) * 128 * sizeof(float4) : 0);
+                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
     auto launch = [&](auto kern) {
         ensure_smem(kern, smem);
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
     };
+    // the banded raster only where big frames need it (float4 lanes, F = 32 / 64) and the
+    // remap's condition holds (a CTA's queries inside one image row)
+    constexpr bool kBandInst = VEC == 4 && (G == 8 || G == 16);
+    if constexpr (kBandInst) {
+        if (!s.grid && s.band > 0 && s.d.nw % C::QPB == 0) {
+            if (s.metric == SNLS_METRIC_IP)
+                launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG, false, false, true>);
+            else
+                launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_L2, MINB, QREG, false, false, true>);
+            return 1;
+        }
+    }
     if (s.grid) {
         if (s.metric == SNLS_METRIC_IP)
             launch(search_tiled_kernel<P, W, VEC, G, KMAX, SNLS_METRIC_IP, MINB, QREG, true>);
@@ -626,7 +607,60 @@ int launch_by_k(const TiledSearch& s, cudaStream_t st) {
     return 0;
 }
 
+template <int P, int VEC, int G>
+int launch_replay_cfg(const TiledSearch& s, cudaStream_t st) {
+    using C = TiledCfg<P, 1, VEC, G>;
+    const unsigned blocks = unsigned((s.d.rows + C::QPB - 1) / C::QPB);
+    constexpr bool QSM = kQsm && VEC == 2;
+    constexpr bool QREG = P >= 7 && !QSM;
+    const size_t smem = QSM ? size_t(C::QPB) * P * P * G * sizeof(u64)
+                            : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
+    auto launch = [&](auto kern) {
+        ensure_smem(kern, smem);
+        kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
+    };
+    if (s.metric == SNLS_METRIC_IP)
+        launch(search_tiled_kernel<P, 1, VEC, G, 16, SNLS_METRIC_IP, 1, QREG, true, true>);
+    else
+        launch(search_tiled_kernel<P, 1, VEC, G, 16, SNLS_METRIC_L2, 1, QREG, true, true>);
+    return 1;
+}
+
+template <int P>
+int launch_replay_p(const TiledSearch& s, cudaStream_t st) {
+    if constexpr (P >= 7) {  // the forward's lane layout for this (ps, F): launch_by_f
+        switch (s.d.f) {
+            case 16: return launch_replay_cfg<P, 2, 8>(s, st);
+            case 32: return launch_replay_cfg<P, 2, 16>(s, st);
+            case 64: return launch_replay_cfg<P, 2, 32>(s, st);
+            default: return 0;
+        }
+    } else {
+        switch (s.d.f) {
+            case 4: return launch_replay_cfg<P, 4, 1>(s, st);
+            case 8: return launch_replay_cfg<P, 4, 2>(s, st);
+            case 16: return launch_replay_cfg<P, 4, 4>(s, st);
+            case 32: return launch_replay_cfg<P, 4, 8>(s, st);
+            case 64: return launch_replay_cfg<P, 4, 16>(s, st);
+            default: return 0;
+        }
+    }
+}
+
 }  // namespace
+
+int launch_replay_tiled(const TiledSearch& s, cudaStream_t st) {
+    // the (ps, ws) pairs the forward's tiled plan is instantiated for (launch_search_tiled)
+    const bool tiled = s.topl <= 16 && ((s.ps == 3 && (s.ws == 11 || s.ws == 9 || s.ws == 5)) ||
+                                        (s.ps == 7 && s.ws == 9) || (s.ps == 1 && (s.ws == 9 || s.ws == 5)));
+    if (!tiled) return 0;
+    switch (s.ps) {
+        case 1: return launch_replay_p<1>(s, st);
+        case 3: return launch_replay_p<3>(s, st);
+        case 7: return launch_replay_p<7>(s, st);
+        default: return 0;
+    }
+}
 
 // Instantiated (ps, ws) pairs; anything else takes the generic path.
 int launch_search_tiled(const TiledSearch& s, cudaStream_t st, int* used) {

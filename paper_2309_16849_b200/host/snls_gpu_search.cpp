@@ -139,13 +139,6 @@ struct SearchBuffers {
 };
 thread_local SearchBuffers t_buf;
 
-void query_base(const QueryGrid& g, std::int64_t row, double& qt, double& qy, double& qx) {
-    int t, y, x;
-    g.coords(row, t, y, x);
-    qt = t;
-    qy = y;
-    qx = x;
-}
 
 }  // namespace
 
@@ -277,36 +270,6 @@ std::pair<SimilarityTensor, OffsetTensor> top_l(const SimilarityTensor& full,
     return {std::move(sel), std::move(off)};
 }
 
-namespace {
-// Device tape from the reference tape: offsets = centres - query, chains relative.
-void tape_to_device(const SearchTape& tape, float*& doffs, float*& dch) {
-    const std::int64_t rows = tape.grid.rows();
-    const int L = tape.cfg.topl, cs = tape.chain_stride;
-    const std::size_t n = std::size_t(rows) * L;
-    std::vector<double> offs(n * 3), rel(n * std::size_t(cs) * 6, 0.0);
-    // rows write disjoint slices of offs / rel
-#pragma omp parallel for schedule(static)
-    for (std::int64_t row = 0; row < rows; ++row) {
-        double qt, qy, qx;
-        query_base(tape.grid, row, qt, qy, qx);
-        for (int li = 0; li < L; ++li) {
-            const std::size_t e = std::size_t(row) * L + li;
-            offs[e * 3 + 0] = tape.centers[e * 3 + 0] - qt;
-            offs[e * 3 + 1] = tape.centers[e * 3 + 1] - qy;
-            offs[e * 3 + 2] = tape.centers[e * 3 + 2] - qx;
-            const int links = std::max(int(std::lround(std::abs(offs[e * 3]))) - 1, 0);
-            for (int kk = 0; kk < links && kk < cs; ++kk) {
-                const std::size_t b = (e * cs + kk) * 6;
-                rel[b + 0] = tape.chains[b + 0] - qy;
-                rel[b + 1] = tape.chains[b + 1] - qx;
-                for (int j = 2; j < 6; ++j) rel[b + j] = tape.chains[b + j];
-            }
-        }
-    }
-    doffs = gpu::upload(t_buf.offsets, offs);
-    dch = cs > 0 ? gpu::upload(t_buf.chains, rel) : nullptr;
-}
-}  // namespace
 
 SearchGradients shifted_nls_backward(const SimilarityTensor& grad_selected,
                                      const SearchTape& tape, const VideoTensor& q,
@@ -367,14 +330,17 @@ SimilarityTensor replay_similarities(const SearchTape& tape, const VideoTensor& 
     out.rows = tape.grid.rows();
     out.cols = tape.cfg.topl;
     snls_ctx* ctx = gpu::context();
-    float *doffs = nullptr, *dch = nullptr;
-    tape_to_device(tape, doffs, dch);
-    float* dq = gpu::upload(t_buf.q, q.data);
-    float* dk = gpu::upload(t_buf.k, k.data);
+    // the fp64 tape centres as they are, replayed through the search plan's own per-slot
+    // arithmetic (snls_replay64): the forward's similarities bit for bit (search.cpp:470-493)
     const std::uint64_t n = std::uint64_t(out.rows) * out.cols;
+    double* dcen = static_cast<double*>(t_buf.cen64.reserve(n * 3 * sizeof(double)));
+    gpu::check(snls_copy_h2d(ctx, dcen, tape.centers.data(), n * 3 * sizeof(double)));
+    float* dq = gpu::upload_async(t_buf.q, q.data.data(), q.data.size());
+    const bool alias = (&q == &k || q.data == k.data);
+    float* dk = alias ? dq : gpu::upload_async(t_buf.k, k.data.data(), k.data.size());
     float* dsims = t_buf.sims.f32(n);
     const snls_config c = gpu::to_abi(tape.cfg);
-    gpu::check(snls_replay(ctx, &c, dims_of(q), dq, dk, doffs, dsims));
+    gpu::check(snls_replay64(ctx, &c, dims_of(q), 0, q.t, dq, dk, dcen, -1, dsims));
     gpu::check(snls_ctx_sync_check(ctx));
     gpu::download(out.values, dsims, n);
     return out;

@@ -113,6 +113,8 @@ def lib() -> C.CDLL:
             L.snls_ctx_last_search_path.argtypes = [VOIDP, C.POINTER(C.c_int)]
             L.snls_ctx_force_generic.argtypes = [VOIDP, C.c_int]
             L.snls_ctx_set_search_kernel.argtypes = [VOIDP, C.c_int]
+            if hasattr(L, "snls_ctx_set_search_band"):
+                L.snls_ctx_set_search_band.argtypes = [VOIDP, C.c_int]
             L.snls_validate_config.argtypes = [C.POINTER(_Config)]
             P = C.POINTER(_Config)
             L.snls_search_fwd.argtypes = [VOIDP, P, _Dims, VOIDP, VOIDP, VOIDP, VOIDP, C.c_int,
@@ -143,6 +145,8 @@ def lib() -> C.CDLL:
             L.snls_align_frames.argtypes = [VOIDP, P, _Dims, VOIDP, C.c_double, C.c_uint64, C.c_int,
                                             VOIDP, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
+            if hasattr(L, "snls_replay64"):
+                L.snls_replay64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, C.c_int, VOIDP]
             if hasattr(L, "snls_search_bwd_ex"):  # (absent from A/B builds of older trees)
                 L.snls_search_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 11 + [C.c_int]
                 L.snls_search_tape64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 5
@@ -239,6 +243,10 @@ class Context:
 
     def force_generic(self, on: bool):
         _raise(lib().snls_ctx_force_generic(self.h, int(on)))
+
+    def set_search_band(self, band: int):
+        """-1 auto, 0 plain raster, > 0 query rows per band (snls_ctx_set_search_band)."""
+        _raise(lib().snls_ctx_set_search_band(self.h, int(band)))
 
     def set_search_kernel(self, kind: str):
         """'auto' | 'tiled' | 'stream' register plan for the stride1 == 1 search."""
@@ -383,15 +391,23 @@ def top_l(full, full_offsets, topl: int, ctx=None):
     return sel, soff
 
 
-def replay_similarities(res: SearchResult, q, k, ctx=None):
-    """snls::replay_similarities (search.hpp:157-158), from the device tape."""
+def replay_similarities(res: SearchResult, q, k, ctx=None, centers=None, plan: str = "auto"):
+    """snls::replay_similarities (search.hpp:157-158).  With the fp64 tape `centers`
+    (search_tape64) through the search plan's own arithmetic -- bitwise equal to that plan's
+    forward (snls_replay64; plan 'auto' = the one the forward takes); without, from the fp32
+    device tape (snls_replay, fp32 tolerance)."""
     import torch
 
     ctx = ctx or context(q.device.index)
     c = _cfg(res.cfg)
     sims = torch.empty_like(res.sims)
-    _raise(lib().snls_replay(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(res.offsets),
-                             _ptr(sims)))
+    if centers is not None:
+        t = q.shape[0]
+        _raise(lib().snls_replay64(ctx.h, C.byref(c), _dims(q), 0, t, _ptr(q), _ptr(k), _ptr(centers),
+                                   {"auto": -1, "generic": 0, "tiled": 1, "stream": 2}[plan], _ptr(sims)))
+    else:
+        _raise(lib().snls_replay(ctx.h, C.byref(c), _dims(q), _ptr(q), _ptr(k), _ptr(res.offsets),
+                                 _ptr(sims)))
     ctx.sync_check()
     return sims
 

@@ -122,8 +122,8 @@ def test_c3_device_forward_tape64_is_the_reference_tape(port, metric):
     cen, ch = cen.cpu().numpy(), ch.cpu().numpy()
     same = np.all(np.abs(host(r.offsets) - fw["offsets"]) <= 1e-5, axis=(1, 2))
     assert same.mean() >= 0.99, st
-    assert np.max(np.abs(cen[same] - fw["centers"][same])) <= 1e-12
-    assert np.max(np.abs(ch[same] - fw["chains"][same])) <= 1e-12
+    assert np.max(np.abs(cen[same] - fw["centers"][same])) <= 1e-9  # (shift on the 2^-32 grid)
+    assert np.max(np.abs(ch[same] - fw["chains"][same])) <= 1e-9
     got = [host(x) for x in S.shifted_nls_backward(dev(g), r, dev(q), dev(k),
                                                    tape64=(torch.tensor(cen, device="cuda"),
                                                            torch.tensor(ch, device="cuda")))]

@@ -34,6 +34,11 @@ FP64_ONLY = {
 }
 
 
+# checks that must pass OUTRIGHT on the GPU adapter (no fp32 waiver): the replay of the fp64
+# tape is bitwise the forward (snls_replay64 through the forward's own plan)
+MUST_PASS = {"test_search.cpp:551": "tape replay reproduces the forward similarities bitwise"}
+
+
 def _run(kind, name):
     exe = os.path.join(BUILD, kind, name)
     if not os.path.exists(exe):
@@ -57,6 +62,9 @@ def test_reference_suite_on_gpu_adapter(name):
     bad = []
     for line in fails:
         where = os.path.basename(line.split()[1])
+        if where in MUST_PASS:
+            bad.append(line + "  [must pass bitwise: " + MUST_PASS[where] + "]")
+            continue
         m = re.search(r"rel=([0-9.eE+-]+|inf|nan)", line)
         if where in FP64_ONLY:
             continue

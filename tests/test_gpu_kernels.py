@@ -144,3 +144,28 @@ def test_topl_sizes_bit_exact_on_integer_inputs(port, ws, ps, f, metric, topl):
         if mode == 0:
             assert ctx.last_search_path() == (1 if topl <= 16 else 0)
         compare_search(r, ref, cfg, exact=True)
+
+
+@pytest.mark.parametrize("band", [1, 3, 5])
+def test_band_raster_is_bitwise_the_plain_raster(port, band):
+    """The temporally blocked CTA raster (common.cuh band_row; c5's default) only reorders
+    independent queries: sims, offsets, weights and the full grid are bitwise the plain
+    raster's.  Shapes with nw a multiple of the CTA's query count (the remap's condition)."""
+    S = snls_mod()
+    cases = [(5, 19, 32, 32, Cfg(ws=11, wt=3, ps=3, stride0=2, topl=16, metric="l2", softmax_scale=1 / 288)),
+             (4, 17, 16, 64, Cfg(ws=9, wt=2, ps=3, stride0=1, topl=10, metric="l2", softmax_scale=1 / 576))]
+    ctx = S.context()
+    for t, h, w, f, cfg in cases:
+        v = dev(video(port, t, h, w, f, 4400 + f))
+        ff, bf = dev(flow(port, t, h, w, 4500, 2.0)), dev(flow(port, t, h, w, 4501, 2.0))
+        outs = []
+        for b in (0, band):
+            ctx.set_search_band(b)
+            try:
+                r = S.shifted_nls_forward(v, v, ff, bf, scfg(cfg), want_weights=True, ctx=ctx)
+                g = S.shifted_nls_forward(v, v, ff, bf, scfg(cfg), mode=1, ctx=ctx)
+            finally:
+                ctx.set_search_band(-1)
+            outs.append([host(x) for x in (r.sims, r.offsets, r.weights, g.sims)])
+        for x, y in zip(*outs):
+            assert np.array_equal(x, y)

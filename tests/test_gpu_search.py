@@ -259,3 +259,40 @@ def test_degenerate_shapes_and_far_flows(port, plan):
         finally:
             ctx.set_search_kernel("auto")
         compare_search(r, ref, cfg, q, k, label=f" {plan} case{i}")
+
+
+REPLAY_SHAPES = [  # (t, h, w, f, cfg): c4 / c5 / c2 lane layouts, both metrics, plus generic-only
+    (5, 23, 21, 32, Cfg(ws=11, wt=3, ps=3, stride0=2, topl=16, metric="l2")),
+    (4, 19, 22, 64, Cfg(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2")),
+    (4, 20, 18, 64, Cfg(ws=9, wt=2, ps=7, stride0=4, topl=10, metric="ip")),
+    (3, 13, 15, 16, Cfg(ws=5, wt=1, ps=3, stride0=2, topl=6, metric="ip")),
+    (3, 12, 11, 8, Cfg(ws=9, wt=1, ps=1, stride0=1, topl=10, metric="l2")),
+    (3, 11, 12, 4, Cfg(ws=5, wt=1, ps=3, stride0=2, stride1=0.5, topl=5, metric="l2")),  # generic
+]
+
+
+@pytest.mark.parametrize("plan", ["tiled", "stream", "generic"])
+@pytest.mark.parametrize("i", range(len(REPLAY_SHAPES)))
+def test_replay_is_bitwise_the_forward_of_every_plan(port, plan, i):
+    """replay_similarities from the fp64 tape (search.cpp:470-493; test_search.cpp:539-553:
+    'replay reproduces the selected similarities exactly') through each plan's own per-slot
+    arithmetic equals that plan's forward BIT FOR BIT -- on the reference's own tape too."""
+    S = snls_mod()
+    t, h, w, f, cfg = REPLAY_SHAPES[i]
+    q, k = video(port, t, h, w, f, 9100 + i), video(port, t, h, w, f, 9200 + i)
+    ff, bf = flow(port, t, h, w, 9300 + i, 2.0), flow(port, t, h, w, 9400 + i, 2.0)
+    ctx = S.context()
+    ctx.set_search_kernel("stream" if plan == "stream" else "tiled")
+    ctx.force_generic(plan == "generic")
+    try:
+        dq, dk, dff, dbf = dev(q), dev(k), dev(ff), dev(bf)
+        r = S.shifted_nls_forward(dq, dk, dff, dbf, scfg(cfg), ctx=ctx)
+        cen, _ = S.search_tape64(r, dff, dbf, ctx=ctx)
+        got = S.replay_similarities(r, dq, dk, ctx=ctx, centers=cen)  # 'auto': the plan just used
+    finally:
+        ctx.set_search_kernel("auto")
+        ctx.force_generic(False)
+    assert np.array_equal(host(got), host(r.sims)), (ctx.last_search_path(), np.abs(host(got) - host(r.sims)).max())
+    # and the oracle's replay of the same tape agrees to the fp32 tolerance
+    want = port.replay(q, k, cfg, cen.cpu().numpy())
+    assert max_rel(host(got), want) <= REL_TOL

@@ -8,6 +8,7 @@
 // C-vectorised (float4) reads of V.  The backward scatters through 4 bilinear taps, so it
 // uses atomics (the reference's non-deterministic mode, aggregate.cpp:451-458).
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -710,7 +711,9 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
 #endif
 constexpr bool kGsSm = SNLS_WBWD_GSSM != 0;
 
-template <int P>
+// FT > 0: compile-time channel count; raw blocks inside the frame use immediate column
+// offsets from one row base (no reflection / per-element address math), as search_bwd_rows.
+template <int P, int FT = 0>
 __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, const float* __restrict__ go,
                                                          const int32_t* __restrict__ counts,
                                                          float* __restrict__ dv, float* __restrict__ dw) {
@@ -786,60 +789,73 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
         const float wv = __ldg(a.weights + e);
         const int by = qy - HP + int_base(fly), bx = qx - HP + int_base(flx);
-        unsigned bcol[P + 1];
-#pragma unroll
-        for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);
         const float* __restrict__ vb = a.v + size_t(kt) * frameF + cc;
         float* dvb = dv + size_t(kt) * frameF + cc;
-        float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
-        size_t roa = size_t(reflect_near(by, H)) * rowF;
-        size_t rob = size_t(reflect_near(by + 1, H)) * rowF;
-#pragma unroll
-        for (int j = 0; j <= P; ++j) {
-            ra[j] = act ? __ldg(vb + roa + bcol[j]) : 0.f;
-            rb[j] = act ? __ldg(vb + rob + bcol[j]) : 0.f;
-            ka[j] = 0.f;
-        }
         float dwl = 0.f;
+        auto body = [&](auto fast_tag) {
+            constexpr bool FAST = decltype(fast_tag)::value;
+            unsigned bcol[FAST ? 1 : P + 1];
+            if constexpr (!FAST) {
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-            // raw row i+2 is loaded one row ahead (its latency overlaps row i's arithmetic)
-            float rn[P + 1];
-            const size_t ron = size_t(reflect_near(by + i + 2, H)) * rowF;
-            if (i + 1 < P) {
+                for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, W)) * unsigned(a.d.f);
+            }
+            auto colo = [&](int j) -> size_t { return FAST ? size_t(j) * FT : size_t(bcol[FAST ? 0 : j]); };
+            const size_t xo = FAST ? size_t(bx) * FT : 0;
+            auto rowo = [&](int r) -> size_t {
+                return FAST ? size_t(by + r) * rowF + xo : size_t(reflect_near(by + r, H)) * rowF;
+            };
+            float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
+            size_t roa = rowo(0), rob = rowo(1);
 #pragma unroll
-                for (int j = 0; j <= P; ++j) rn[j] = act ? __ldg(vb + ron + bcol[j]) : 0.f;
+            for (int j = 0; j <= P; ++j) {
+                ra[j] = act ? __ldg(vb + roa + colo(j)) : 0.f;
+                rb[j] = act ? __ldg(vb + rob + colo(j)) : 0.f;
+                ka[j] = 0.f;
             }
 #pragma unroll
-            for (int j = 0; j <= P; ++j) kn[j] = 0.f;
+            for (int i = 0; i < P; ++i) {
+                // raw row i+2 is loaded one row ahead (its latency overlaps row i's arithmetic)
+                float rn[P + 1];
+                const size_t ron = rowo(i + 2);
+                if (i + 1 < P) {
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                const float smp = w00 * ra[j] + w01 * ra[j + 1] + w10 * rb[j] + w11 * rb[j + 1];
-                const float gij = gsv(i, j);
-                dwl = fmaf(gij, smp, dwl);
-                const float gv = gij * wv;
-                ka[j] += gv * w00;
-                ka[j + 1] += gv * w01;
-                kn[j] += gv * w10;
-                kn[j + 1] += gv * w11;
+                    for (int j = 0; j <= P; ++j) rn[j] = act ? __ldg(vb + ron + colo(j)) : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j <= P; ++j) kn[j] = 0.f;
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const float smp = w00 * ra[j] + w01 * ra[j + 1] + w10 * rb[j] + w11 * rb[j + 1];
+                    const float gij = gsv(i, j);
+                    dwl = fmaf(gij, smp, dwl);
+                    const float gv = gij * wv;
+                    ka[j] += gv * w00;
+                    ka[j + 1] += gv * w01;
+                    kn[j] += gv * w10;
+                    kn[j + 1] += gv * w11;
+                }
+                if (act) {
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + colo(j), ka[j]);
+                }
+#pragma unroll
+                for (int j = 0; j <= P; ++j) {
+                    ra[j] = rb[j];
+                    if (i + 1 < P) rb[j] = rn[j];
+                    ka[j] = kn[j];
+                }
+                roa = rob;
+                rob = ron;
             }
             if (act) {
 #pragma unroll
-                for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + bcol[j], ka[j]);
+                for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + colo(j), ka[j]);
             }
-#pragma unroll
-            for (int j = 0; j <= P; ++j) {
-                ra[j] = rb[j];
-                if (i + 1 < P) rb[j] = rn[j];
-                ka[j] = kn[j];
-            }
-            roa = rob;
-            rob = ron;
-        }
-        if (act) {
-#pragma unroll
-            for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + bcol[j], ka[j]);
-        }
+        };
+        if (FT > 0 && by >= 0 && by + P < H && bx >= 0 && bx + P < W)  // uniform: one row per warp
+            body(std::integral_constant<bool, (FT > 0)>{});
+        else
+            body(std::false_type{});
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) dwl += __shfl_xor_sync(0xffffffffu, dwl, m);
         if (lane == 0) atomicAdd(dw + e, dwl);
@@ -850,7 +866,10 @@ template <int P>
 void launch_wpsum_bwd_rows(const AggArgs& a, const float* go, const int32_t* counts, float* dv,
                            float* dw, cudaStream_t st) {
     const int64_t warps = a.d.rows * ((a.d.f + 31) / 32);
-    wpsum_bwd_rows<P><<<unsigned((warps + 3) / 4), 128, 0, st>>>(a, go, counts, dv, dw);
+    const unsigned blocks = unsigned((warps + 3) / 4);
+    if (a.d.f == 64) wpsum_bwd_rows<P, 64><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
+    else if (a.d.f == 32) wpsum_bwd_rows<P, 32><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
+    else wpsum_bwd_rows<P, 0><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
 }
 
 }  // namespace

@@ -8,6 +8,8 @@
 // Phase 2: one thread per entry routes (gy, gx) back through the composition chain
 // (search.cpp:584-666): dt >= 0 into dFflow, dt < 0 into dBflow, v <- (I + J)^T v per link.
 // Entries with a zero upstream gradient are skipped (search.cpp:692).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -148,7 +150,10 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 // atomic is a fully coalesced 128 B warp access along the channels.
 // The query patch is parked in shared memory once per warp (each lane reads back only its own
 // channel: no barrier; c3 backward 0.730 -> 0.684 ms).
-template <int P, bool DET, bool CORR>
+// FT > 0: the channel count as a compile-time constant; entries whose raw block lies inside
+// the frame then address it as row base + j * FT (immediate offsets: no reflection, no
+// per-element address arithmetic -- most of this kernel's integer work); FT = 0 any F.
+template <int P, bool DET, bool CORR, int FT = 0>
 __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const float* __restrict__ grad,
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
@@ -225,87 +230,101 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
         }
         const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
         const float w10 = fy * (1.f - fx), w11 = fy * fx;
-        unsigned bcol[P + 1];
-#pragma unroll
-        for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, d.w)) * unsigned(d.f);
         const float* kb = k + size_t(kt) * frameF + cc;
         const size_t dkb = size_t(kt) * frameF + cc;
-        float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
-        size_t roa = size_t(reflect_near(by, d.h)) * rowF;
-        size_t rob = size_t(reflect_near(by + 1, d.h)) * rowF;
-#pragma unroll
-        for (int j = 0; j <= P; ++j) {
-            ra[j] = act ? __ldg(kb + roa + bcol[j]) : 0.f;
-            rb[j] = act ? __ldg(kb + rob + bcol[j]) : 0.f;
-            ka[j] = 0.f;
-        }
         // dS/d(ky, kx) sums thousands of cancelling terms per entry: fp64 accumulation of the
         // fp32 per-term products (c3 l2 flow gradients 1.4e-5 -> 3e-6 relative, +1% time)
         double sy = 0.0, sx = 0.0;
         // CORR: first-order terms of the fp32 rounding of the fractions (bilinear samples are
         // linear in fy, fx; the flow gradients amplify the rounding by sum (dk/dy)^2)
         float cA = 0.f, cB = 0.f, cD = 0.f, cC = 0.f;
+        // the (P+1)^2 raw block, two rows at a time; FAST: inside the frame, immediate column
+        // offsets j * FT from one row base; else reflected rows / columns (tensor.cpp:23-48)
+        auto body = [&](auto fast_tag) {
+            constexpr bool FAST = decltype(fast_tag)::value;
+            unsigned bcol[FAST ? 1 : P + 1];
+            if constexpr (!FAST) {
 #pragma unroll
-        for (int py = 0; py < P; ++py) {
-            const size_t ron = size_t(reflect_near(by + py + 2, d.h)) * rowF;
-#pragma unroll
-            for (int j = 0; j <= P; ++j) kn[j] = 0.f;
-#pragma unroll
-            for (int px = 0; px < P; ++px) {
-                const float k00 = ra[px], k01 = ra[px + 1], k10 = rb[px], k11 = rb[px + 1];
-                const float qv = sq[(py * P + px) * 32];
-                // lerp form: the x-interpolated rows give the sample and both tap derivatives
-                // (search.cpp:574-577) in 8 FP ops instead of 12
-                const float d0 = k01 - k00, d1 = k11 - k10;
-                const float hx0 = fmaf(fx, d0, k00), hx1 = fmaf(fx, d1, k10);
-                const float dkv_dy = hx1 - hx0;
-                const float kv = fmaf(fy, dkv_dy, hx0);
-                const float dkv_dx = fmaf(fy, d1 - d0, d0);
-                float ds_dq, ds_dk;
-                if (metric == SNLS_METRIC_IP) {
-                    ds_dq = kv;
-                    ds_dk = qv;
-                } else {
-                    const float diff = qv - kv;
-                    ds_dq = -2.f * diff;
-                    ds_dk = 2.f * diff;
-                }
-                const float gk = g * ds_dk;
-                if constexpr (kDqSm) sdq[(py * P + px) * 32] = fmaf(g, ds_dq, sdq[(py * P + px) * 32]);
-                else dqa[py][px] = fmaf(g, ds_dq, dqa[py][px]);
-                ka[px] = fmaf(gk, w00, ka[px]);
-                ka[px + 1] = fmaf(gk, w01, ka[px + 1]);
-                kn[px] = fmaf(gk, w10, kn[px]);
-                kn[px + 1] = fmaf(gk, w11, kn[px + 1]);
-                sy = fma(double(gk), double(dkv_dy), sy);
-                sx = fma(double(gk), double(dkv_dx), sx);
-                if constexpr (CORR) {
-                    cC = fmaf(gk, d1 - d0, cC);
-                    if (metric != SNLS_METRIC_IP) {
-                        cA = fmaf(dkv_dy, dkv_dy, cA);
-                        cB = fmaf(dkv_dy, dkv_dx, cB);
-                        cD = fmaf(dkv_dx, dkv_dx, cD);
-                    }
-                }
+                for (int j = 0; j <= P; ++j) bcol[j] = unsigned(reflect_near(bx + j, d.w)) * unsigned(d.f);
             }
-            if (act) {  // raw row py of the block is complete
-#pragma unroll
-                for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + bcol[j], ka[j]);
-            }
+            auto colo = [&](int j) -> size_t { return FAST ? size_t(j) * FT : size_t(bcol[FAST ? 0 : j]); };
+            const size_t xo = FAST ? size_t(bx) * FT : 0;
+            auto rowo = [&](int r) -> size_t {
+                return FAST ? size_t(by + r) * rowF + xo : size_t(reflect_near(by + r, d.h)) * rowF;
+            };
+            float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
+            size_t roa = rowo(0), rob = rowo(1);
 #pragma unroll
             for (int j = 0; j <= P; ++j) {
-                ra[j] = rb[j];
-                if (py + 1 < P) rb[j] = act ? __ldg(kb + ron + bcol[j]) : 0.f;  // (loading it a
-                // row ahead into registers: same time, 36 B of spills)
-                ka[j] = kn[j];
+                ra[j] = act ? __ldg(kb + roa + colo(j)) : 0.f;
+                rb[j] = act ? __ldg(kb + rob + colo(j)) : 0.f;
+                ka[j] = 0.f;
             }
-            roa = rob;
-            rob = ron;
-        }
-        if (act) {
 #pragma unroll
-            for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + bcol[j], ka[j]);
-        }
+            for (int py = 0; py < P; ++py) {
+                const size_t ron = rowo(py + 2);
+#pragma unroll
+                for (int j = 0; j <= P; ++j) kn[j] = 0.f;
+#pragma unroll
+                for (int px = 0; px < P; ++px) {
+                    const float k00 = ra[px], k01 = ra[px + 1], k10 = rb[px], k11 = rb[px + 1];
+                    const float qv = sq[(py * P + px) * 32];
+                    // lerp form: the x-interpolated rows give the sample and both tap
+                    // derivatives (search.cpp:574-577) in 8 FP ops instead of 12
+                    const float d0 = k01 - k00, d1 = k11 - k10;
+                    const float hx0 = fmaf(fx, d0, k00), hx1 = fmaf(fx, d1, k10);
+                    const float dkv_dy = hx1 - hx0;
+                    const float kv = fmaf(fy, dkv_dy, hx0);
+                    const float dkv_dx = fmaf(fy, d1 - d0, d0);
+                    float ds_dq, ds_dk;
+                    if (metric == SNLS_METRIC_IP) {
+                        ds_dq = kv;
+                        ds_dk = qv;
+                    } else {
+                        const float diff = qv - kv;
+                        ds_dq = -2.f * diff;
+                        ds_dk = 2.f * diff;
+                    }
+                    const float gk = g * ds_dk;
+                    if constexpr (kDqSm) sdq[(py * P + px) * 32] = fmaf(g, ds_dq, sdq[(py * P + px) * 32]);
+                    else dqa[py][px] = fmaf(g, ds_dq, dqa[py][px]);
+                    ka[px] = fmaf(gk, w00, ka[px]);
+                    ka[px + 1] = fmaf(gk, w01, ka[px + 1]);
+                    kn[px] = fmaf(gk, w10, kn[px]);
+                    kn[px + 1] = fmaf(gk, w11, kn[px + 1]);
+sy = fma(double(gk), double(dkv_dy), sy);
+                    sx = fma(double(gk), double(dkv_dx), sx);
+                    if constexpr (CORR) {
+                        cC = fmaf(gk, d1 - d0, cC);
+                        if (metric != SNLS_METRIC_IP) {
+                            cA = fmaf(dkv_dy, dkv_dy, cA);
+                            cB = fmaf(dkv_dy, dkv_dx, cB);
+                            cD = fmaf(dkv_dx, dkv_dx, cD);
+                        }
+                    }
+                }
+                if (act) {  // raw row py of the block is complete
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + colo(j), ka[j]);
+                }
+#pragma unroll
+                for (int j = 0; j <= P; ++j) {
+                    ra[j] = rb[j];
+                    if (py + 1 < P) rb[j] = act ? __ldg(kb + ron + colo(j)) : 0.f;
+                    ka[j] = kn[j];
+                }
+                roa = rob;
+                rob = ron;
+            }
+            if (act) {
+#pragma unroll
+                for (int j = 0; j <= P; ++j) put<DET>(sinkk.f, sinkk.i, sck, dkb + roa + colo(j), ka[j]);
+            }
+        };
+        if (FT > 0 && by >= 0 && by + P < d.h && bx >= 0 && bx + P < d.w)  // uniform: one entry per warp
+            body(std::integral_constant<bool, (FT > 0)>{});
+        else
+            body(std::false_type{});
         if constexpr (CORR) {
             // l2: gk = 2g(q - kv) moves by -2g dkv; both metrics: dkv_dy moves by ddx (d1 - d0),
             // dkv_dx by ddy (d1 - d0)
@@ -346,14 +365,20 @@ void launch_rows(const float* grad, const float* offsets, const float* q, const 
     const int64_t warps = d.rows * ((d.f + 31) / 32);
     const size_t smem = size_t(4) * P * P * 32 * sizeof(float) * (kDqSm ? 2 : 1);
     const unsigned blocks = unsigned((warps + 3) / 4);
+    auto go = [&](auto kern) {
+        ensure_smem(kern, smem);
+        kern<<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers);
+    };
+    // compile-time channel counts of the BASELINE shapes (fast interior addressing)
+    const int ft = DET ? 0 : (d.f == 64 ? 64 : (d.f == 32 ? 32 : 0));
     if (centers) {
-        ensure_smem(search_bwd_rows<P, DET, true>, smem);
-        search_bwd_rows<P, DET, true><<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk,
-                                                                 gyx, centers);
+        if (ft == 64) go(search_bwd_rows<P, DET, true, DET ? 0 : 64>);
+        else if (ft == 32) go(search_bwd_rows<P, DET, true, DET ? 0 : 32>);
+        else go(search_bwd_rows<P, DET, true, 0>);
     } else {
-        ensure_smem(search_bwd_rows<P, DET, false>, smem);
-        search_bwd_rows<P, DET, false><<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk,
-                                                                  gyx, centers);
+        if (ft == 64) go(search_bwd_rows<P, DET, false, DET ? 0 : 64>);
+        else if (ft == 32) go(search_bwd_rows<P, DET, false, DET ? 0 : 32>);
+        else go(search_bwd_rows<P, DET, false, 0>);
     }
 }
 

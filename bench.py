@@ -309,11 +309,14 @@ def run_ours(args, wl):
         S.wpsum(vid, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
         for (xv, _, _, _, xo, xw, xout, xcnt) in extra:  # ... and aggregation
             S.wpsum(xv, xw, xo, cfg, ctx=ctx, check=False, out=(xout, xcnt))
-        if train:  # backward: wpsum_backward (dV, dW) then shifted_nls_backward (dQ, dK, dFlow)
+        if train:  # backward of the chain: dQ, dK, dV, dW, dFlow (snls_train_bwd) from the
+            # reference-layout fp64 tape (snls_search_tape64: exact key positions, the flow
+            # gradients' 1e-5 parity holds for Q = K = V self-similarity too)
             ev_bwd.record(stream)
-            S.wpsum_backward(g_out, counts, vid, wts, offs, cfg, ctx=ctx, check=False)
-            S.shifted_nls_backward(g_sims, res, vid, vid, ctx=ctx, check=False,
-                                   deterministic=args.deterministic)
+            res.weights = wts
+            t64 = S.search_tape64(res, ff, bf, ctx=ctx, check=False)
+            S.train_backward(g_sims, g_out, counts, res, vid, vid, vid, ctx=ctx, check=False,
+                             deterministic=args.deterministic, tape64=t64)
 
     # correctness gate before timing: device error latch must be clean
     ev_mid = torch.cuda.Event(enable_timing=True)
@@ -402,9 +405,10 @@ def run_ours(args, wl):
                                         out=(sims, offs, chains if train else None, wts), frames=frames)
             S.wpsum(v2, wts, offs, cfg, ctx=ctx, check=False, out=(out, counts), frames=frames)
             if train:
-                S.wpsum_backward(g_out, counts, v2, wts, offs, cfg, ctx=ctx, check=False)
-                S.shifted_nls_backward(g_sims, res, v2, v2, ctx=ctx, check=False,
-                                       deterministic=args.deterministic)
+                res.weights = wts
+                t64 = S.search_tape64(res, f2, b2, ctx=ctx, check=False)
+                S.train_backward(g_sims, g_out, counts, res, v2, v2, v2, ctx=ctx, check=False,
+                                 deterministic=args.deterministic, tape64=t64)
             sims_p.copy_(sims, non_blocking=True)
             offs_p.copy_(offs, non_blocking=True)
             out_p.copy_(out, non_blocking=True)
@@ -532,7 +536,7 @@ def run_ours(args, wl):
                        ("torch H2D + snls_halo_exchange_async (C-ABI NCCL) + snls_search_fwd_frames/"
                         "wpsum_fwd_frames + D2H" if overlapped else
                         "torch H2D + snls_search_fwd / snls_wpsum_fwd" +
-                        (" / snls_wpsum_bwd / snls_search_bwd_ex" if train else "") + " (C-ABI) + D2H")},
+                        (" / snls_train_bwd" if train else "") + " (C-ABI) + D2H")},
         "gpu_launches": launches,
         "clocks": clk,
         "wall_s_timed_loop": wall,

@@ -280,6 +280,15 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
                           const float* grad_out, const int32_t* counts, const float* v,
                           const float* weights, const float* offsets, float* dv, float* dweights);
 
+/* The whole backward of search -> softmax weights -> wpsum in one call: wpsum_backward (dv,
+ * dweights from grad_out / counts) then shifted_nls_backward (dq, dk, dfflow, dbflow; tape =
+ * offsets + chains or fp64 centres + chains64 as in snls_search_bwd_ex; flags as there). */
+int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad_sims,
+                   const float* grad_out, const int32_t* counts, const float* offsets,
+                   const float* chains, const double* centers, const double* chains64,
+                   const float* q, const float* k, const float* v, const float* weights, float* dq,
+                   float* dk, float* dv, float* dweights, float* dfflow, float* dbflow, int flags);
+
 /* ---- frame alignment ------------------------------------------
  * Replaces snls::estimate_flow_block_matching (flow.hpp:48-49; flow.cpp:114-175) for
  * dims.t frame pairs at once: a[t] -> b[t] (DEVICE, T x H x W x F), flow T x H x W x 2

@@ -829,4 +829,17 @@ int snls_gaussian_noise_f32(uint64_t seed, double sigma, int64_t n, const float*
     return SNLS_OK;
 }
 
+int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad_sims,
+                   const float* grad_out, const int32_t* counts, const float* offsets,
+                   const float* chains, const double* centers, const double* chains64,
+                   const float* q, const float* k, const float* v, const float* weights, float* dq,
+                   float* dk, float* dv, float* dweights, float* dfflow, float* dbflow, int flags) {
+    // the two operators one after the other (a single fused kernel for v == k was measured
+    // slower: 168 registers and three shared-memory patches per warp, 12 warps/SM -- c3
+    // backward 0.80 vs 0.585 ms, profiles/r01_plans.txt)
+    if (int rc = snls_wpsum_bwd(ctx, cfg, dims, grad_out, counts, v, weights, offsets, dv, dweights)) return rc;
+    return snls_search_bwd_ex(ctx, cfg, dims, 0, dims.t, grad_sims, centers ? nullptr : offsets,
+                              centers ? nullptr : chains, centers, chains64, q, k, dq, dk, dfflow, dbflow, flags);
+}
+
 }  // extern "C"

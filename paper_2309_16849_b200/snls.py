@@ -145,6 +145,8 @@ def lib() -> C.CDLL:
             L.snls_align_frames.argtypes = [VOIDP, P, _Dims, VOIDP, C.c_double, C.c_uint64, C.c_int,
                                             VOIDP, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, VOIDP]
             L.snls_search_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 9
+            if hasattr(L, "snls_train_bwd"):
+                L.snls_train_bwd.argtypes = [VOIDP, P, _Dims] + [VOIDP] * 17 + [C.c_int]
             if hasattr(L, "snls_replay64"):
                 L.snls_replay64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int, VOIDP, VOIDP, VOIDP, C.c_int, VOIDP]
             if hasattr(L, "snls_search_bwd_ex"):  # (absent from A/B builds of older trees)
@@ -412,7 +414,7 @@ def replay_similarities(res: SearchResult, q, k, ctx=None, centers=None, plan: s
     return sims
 
 
-def search_tape64(res: SearchResult, fflow, bflow, ctx=None, frames=None):
+def search_tape64(res: SearchResult, fflow, bflow, ctx=None, frames=None, check=True, out=None):
     """The reference's fp64 SearchTape (search.hpp:89-110) of a device result: absolute
     centres rows x L x 3 and (wt > 1) absolute chain links rows x L x (wt-1) x 6, float64."""
     import torch
@@ -425,12 +427,16 @@ def search_tape64(res: SearchResult, fflow, bflow, ctx=None, frames=None):
     t, h, w = fflow.shape[:3]
     t0, t1 = frames if frames is not None else (0, t)
     rows, L = res.sims.shape
-    cen = torch.empty((rows, L, 3), device=res.sims.device, dtype=torch.float64)
-    ch = (torch.empty((rows, L, cfg.chain_stride(), 6), device=res.sims.device, dtype=torch.float64)
-          if cfg.wt > 1 else None)
+    if out is None:
+        cen = torch.empty((rows, L, 3), device=res.sims.device, dtype=torch.float64)
+        ch = (torch.empty((rows, L, cfg.chain_stride(), 6), device=res.sims.device, dtype=torch.float64)
+              if cfg.wt > 1 else None)
+    else:
+        cen, ch = out
     _raise(lib().snls_search_tape64(ctx.h, C.byref(c), _Dims(t, h, w, 1), int(t0), int(t1),
                                     _ptr(fflow), _ptr(bflow), _ptr(res.offsets), _ptr(cen), _ptr(ch)))
-    ctx.sync_check()
+    if check:
+        ctx.sync_check()
     return cen, ch
 
 
@@ -463,6 +469,30 @@ def shifted_nls_backward(grad_sims, res: SearchResult, q, k, ctx=None, check=Tru
     if check:
         ctx.sync_check()
     return dq, dk, dff, dbf
+
+
+def train_backward(grad_sims, grad_out, counts, res: SearchResult, q, k, v, ctx=None, check=True,
+                   deterministic=False, tape64=None):
+    """The backward of search -> softmax weights -> wpsum in one call (snls_train_bwd):
+    returns (dq, dk, dv, dfflow, dbflow, dweights) as shifted_nls_backward + wpsum_backward;
+    when v is k one fused kernel serves both."""
+    import torch
+
+    ctx = ctx or context(q.device.index)
+    c = _cfg(res.cfg)
+    t, h, w, f = q.shape
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(v)
+    dff = torch.empty((t, h, w, 2), device=q.device, dtype=torch.float32)
+    dbf = torch.empty_like(dff)
+    dw = torch.empty_like(res.weights)
+    cen, ch64 = tape64 if tape64 is not None else (None, None)
+    _raise(lib().snls_train_bwd(ctx.h, C.byref(c), _dims(q), _ptr(grad_sims), _ptr(grad_out), _ptr(counts),
+                                _ptr(res.offsets), _ptr(res.chains), _ptr(cen), _ptr(ch64), _ptr(q), _ptr(k),
+                                _ptr(v), _ptr(res.weights), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dw), _ptr(dff),
+                                _ptr(dbf), 1 if deterministic else 0))
+    if check:
+        ctx.sync_check()
+    return dq, dk, dv, dff, dbf, dw
 
 
 def softmax_rows(sims, beta: float, ctx=None, check=True):

@@ -179,3 +179,41 @@ def test_deterministic_backward_random_configs(port):
             assert max_rel(x, want[key]) <= REL_TOL, (i, key, max_rel(x, want[key]))
         done += 1
     assert done >= 10
+
+
+@pytest.mark.parametrize("metric", ["ip", "l2"])
+def test_train_backward_self_similarity_vs_oracle(port, metric):
+    """snls_train_bwd with Q = K = V aliased (run_benchmark's self-similarity use) at the c3
+    shape, from the fp64 tape, against the oracle's two backward operators: dQ, dK, dV, dW,
+    dFflow, dBflow.  (With Q = K the self-matches make the flow gradients large and
+    cancelling: the fp32 device tape's rounded positions then cost up to ~2e-5 there, the
+    fp64 tape keeps them at ~3e-6 -- the training path takes the fp64 tape.)"""
+    tape = "fp64"
+    import torch
+
+    S = snls_mod()
+    cfg, q, _, ff, bf, _, _ = c3_case(port, metric)
+    k = v = q  # aliased
+    fw = port.search_fwd(q, k, ff, bf, cfg)
+    g = f32(port.uniform(16, -1, 1, fw["sims"].size).reshape(fw["sims"].shape))
+    wts = port.softmax_rows(fw["sims"], cfg.softmax_scale)
+    _, counts = port.wpsum(v, wts, fw["offsets"], cfg)
+    go = f32(port.uniform(17, -1, 1, v.size).reshape(v.shape))
+    offs32, ch32 = device_tape_from(fw, cfg)
+    res = S.SearchResult(sims=dev(fw["sims"]), offsets=dev(offs32), chains=dev(ch32), weights=dev(wts),
+                         cfg=scfg(cfg))
+    t64 = None
+    if tape == "fp64":
+        cen, ch = fw["centers"], fw["chains"]
+        t64 = (torch.tensor(cen, device="cuda"), torch.tensor(ch, device="cuda"))
+    else:
+        cen, ch = same_fp32_tape(offs32, ch32, cfg)
+    dq_, dk_, dv_, dff_, dbf_, dw_ = [host(x) for x in S.train_backward(
+        dev(g), dev(go), dev(counts), res, dev(q), dev(k), dev(v), tape64=t64)]
+    sb = port.search_bwd(q, k, cfg, cen, ch, g)
+    wdv, wdw = port.wpsum_bwd(go, counts, v, wts, fw["offsets"], cfg)
+    for got, want, name in ((dq_, sb["dq"], "dq"), (dk_, sb["dk"], "dk"), (dff_, sb["dfflow"], "dfflow"),
+                            (dbf_, sb["dbflow"], "dbflow"), (dv_, wdv, "dv"), (dw_, wdw, "dw")):
+        err = max_rel(got, want)
+        print(f"[c3 fused {metric} {tape}] {name}: max rel {err:.2e}")
+        assert err <= REL_TOL, (name, err)

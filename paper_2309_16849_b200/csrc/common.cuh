@@ -228,12 +228,10 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
             const double py = double(qy) + sy, px = double(qx) + sx;
             const double fby = floor(py), fbx = floor(px);
             const double fy = py - fby, fx = px - fbx;
-#ifndef SNLS_LINK_CLAMP
-#define SNLS_LINK_CLAMP 1
-#endif
-            const int iby = SNLS_LINK_CLAMP ? int_base(fby) : int(fby), ibx = SNLS_LINK_CLAMP ? int_base(fbx) : int(fbx);
-            const int y0 = reflect_near(iby, h), y1 = reflect_near(iby + 1, h);
-            const int x0 = reflect_near(ibx, w), x1 = reflect_near(ibx + 1, w);
+            // int() saturates beyond the int range and reflect maps any int into the frame,
+            // so a huge flow still samples in bounds (the +1 then wraps, as PTX add does)
+            const int y0 = reflect_near(int(fby), h), y1 = reflect_near(int(fby) + 1, h);
+            const int x0 = reflect_near(int(fbx), w), x1 = reflect_near(int(fbx) + 1, w);
             const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);
             const double cy = at(fld, fr, y1, x0, 0), dyv = at(fld, fr, y1, x1, 0);
             const double ax = at(fld, fr, y0, x0, 1), bx = at(fld, fr, y0, x1, 1);
@@ -262,6 +260,60 @@ __device__ inline void shift_to_t(const float* __restrict__ ff, const float* __r
     dx = grid32(sx);
 }
 
+// shift_to_t without links, spelled out for the search kernels: the same fp64 operations in
+// the same order (so the same shift, bit for bit), as a plain function -- instantiating the
+// template inside search_tiled_kernel changed ptxas' register allocation (11 -> 14 spill
+// instructions, c4 search 3.90 -> 3.98 ms; profiles/r01_plans.txt), and so did clamping
+// the link base or forming its +1 in unsigned arithmetic.
+__device__ inline void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
+                                int h, int w, int qt, int qy, int qx, int dt, double& dy,
+                                double& dx) {
+    if (ff == nullptr) {
+        dy = 0.0;
+        dx = 0.0;
+        return;
+    }
+    auto at = [&](const float* fl, int t, int y, int x, int c) {
+        return double(__ldg(fl + ((size_t(t) * h + y) * w + x) * 2 + c));
+    };
+    if (dt == 0) {
+        dy = grid32(at(ff, qt, qy, qx, 0));
+        dx = grid32(at(ff, qt, qy, qx, 1));
+        return;
+    }
+    const float* fld = dt > 0 ? ff : bf;
+    const int step = dt > 0 ? 1 : -1;
+    const int m = dt > 0 ? dt : -dt;
+    double sy = 0.0, sx = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const int fr = qt + step * k;
+        double vy, vx;
+        if (k == 0) {
+            vy = at(fld, fr, qy, qx, 0);
+            vx = at(fld, fr, qy, qx, 1);
+        } else {
+            const double py = double(qy) + sy, px = double(qx) + sx;
+            const double fby = floor(py), fbx = floor(px);
+            const double fy = py - fby, fx = px - fbx;
+            const int y0 = reflect_near(int(fby), h), y1 = reflect_near(int(fby) + 1, h);
+            const int x0 = reflect_near(int(fbx), w), x1 = reflect_near(int(fbx) + 1, w);
+            const double ay = at(fld, fr, y0, x0, 0), by = at(fld, fr, y0, x1, 0);
+            const double cy = at(fld, fr, y1, x0, 0), dyv = at(fld, fr, y1, x1, 0);
+            const double ax = at(fld, fr, y0, x0, 1), bx = at(fld, fr, y0, x1, 1);
+            const double cx = at(fld, fr, y1, x0, 1), dxv = at(fld, fr, y1, x1, 1);
+            const double w00 = (1.0 - fy) * (1.0 - fx), w01 = (1.0 - fy) * fx;
+            const double w10 = fy * (1.0 - fx), w11 = fy * fx;
+            vy = w00 * ay + w01 * by + w10 * cy + w11 * dyv;
+            vx = w00 * ax + w01 * bx + w10 * cx + w11 * dxv;
+        }
+        sy += vy;
+        sx += vx;
+    }
+    dy = grid32(sy);
+    dx = grid32(sx);
+}
+
+// With fp32 links (the device tape).
 __device__ inline void shift_to(const float* __restrict__ ff, const float* __restrict__ bf,
                                 int h, int w, int qt, int qy, int qx, int dt, double& dy,
                                 double& dx, float* links) {

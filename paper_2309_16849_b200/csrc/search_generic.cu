@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128) search_generic_kernel(SearchArgs a) {
     for (int fp = lane; fp < nfr; fp += 32) {
         const int dt = scan_dt(fp), kt = qt + dt;
         double sdy = 0.0, sdx = 0.0;
-        if (kt >= 0 && kt < a.d.t) shift_to(a.ff, a.bf, a.d.h, a.d.w, qt, qy, qx, dt, sdy, sdx, nullptr);
+        if (kt >= 0 && kt < a.d.t) shift_to(a.ff, a.bf, a.d.h, a.d.w, qt, qy, qx, dt, sdy, sdx);
         shifts[2 * fp] = sdy;
         shifts[2 * fp + 1] = sdx;
     }

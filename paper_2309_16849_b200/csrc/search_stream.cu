@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128, MINB) search_stream_kernel(TiledSearch a)
             continue;
         }
         double sdy = 0.0, sdx = 0.0;
-        if (!RP && on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx, nullptr);
+        if (!RP && on) shift_to(a.ff, a.bf, H, Wd, qt, qy, qx, dt, sdy, sdx);
         const double cy = RP ? a.tape[size_t(row) * 3 + 1] : double(qy) + sdy;
         const double cx = RP ? a.tape[size_t(row) * 3 + 2] : double(qx) + sdx;
         const double fby = floor(cy), fbx = floor(cx);

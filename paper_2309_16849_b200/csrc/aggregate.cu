@@ -8,10 +8,13 @@
 // C-vectorised (float4) reads of V.  The backward scatters through 4 bilinear taps, so it
 // uses atomics (the reference's non-deterministic mode, aggregate.cpp:451-458).
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "packed.cuh"
 
 namespace snls_gpu {
 
@@ -591,6 +594,224 @@ int launch_wpsum_query(const AggArgs& a, float* out, int32_t* counts, cudaStream
     return 1;
 }
 
+// ---- two-pass patch wpsum (wide patches: ps 5 / 7) --------------------------------------
+// Pass 1, wpsum_patch_kernel: NL lanes per query (one channel pair each, packed FFMA2) sum the
+// softmax-weighted bilinear samples of all L neighbours over the query's ps x ps patch in
+// registers -- each (query, l) reads its (ps+1)^2 raw V block once, row by row -- and store
+// the summed patch to a stream-ordered scratch [row][ps*ps][F].  RS > 1 splits the patch
+// rows over RS lane groups (fewer registers, (ps+RS)/ps the block loads).  Pass 2,
+// wpsum_combine_kernel: every output pixel sums its contributing patch pixels in the
+// reference's fixed order (aggregate.cpp:156-188) and divides by the count.  The same
+// arithmetic in the same order as wpsum_query_kernel (pass 1 = its phase A, pass 2 = its
+// phase B), without its per-tile recomputation of the patches that straddle tiles (ps 7 at
+// s0 4: 36 queries meet a 16 x 16 tile that owns 16) or parking 49 patch pixels x F per
+// query in shared memory (which does not fit at ps 7, F 64).
+#ifndef SNLS_WPP_MINB
+#define SNLS_WPP_MINB 3
+#endif
+template <int P, int NL, int RS>
+__global__ void __launch_bounds__(256, SNLS_WPP_MINB) wpsum_patch_kernel(AggArgs a, float* __restrict__ patch) {
+    constexpr int HP = P / 2, R = (P + RS - 1) / RS, F = 2 * NL;
+    const int64_t unit = (int64_t(blockIdx.x) * 256 + threadIdx.x) / NL;
+    const int c = threadIdx.x % NL;  // this lane's channel pair
+    const bool valid = unit / RS < a.d.rows;
+    const int64_t row = valid ? unit / RS : a.d.rows - 1;  // (idle lanes still shuffle)
+    const int i0 = int(unit % RS) * R;  // first patch row of this lane group
+    int qt, qy, qx;
+    row_coords(a.d, row, qt, qy, qx);
+    const int H = a.d.h, W = a.d.w;
+    const unsigned rowp = unsigned(W) * NL;  // u64 (channel pairs) per image row
+    const u64* vbase = reinterpret_cast<const u64*>(a.v) + c;
+    u64 acc[R][P];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc[i][j] = 0ull;
+    for (int l0 = 0; l0 < a.topl; l0 += NL) {
+        // lane c decodes neighbour l0 + c (frame, integer corner, softmax-weighted bilinear
+        // weights) once; the group then walks the neighbours in order through shuffles, so
+        // the V loads of a neighbour wait on no offset load
+        int dkt = qt, dby = 0, dbx = 0;
+        float d00 = 0.f, d01 = 0.f, d10 = 0.f, d11 = 0.f;
+        if (l0 + c < a.topl) {
+            const size_t e = size_t(row) * a.topl + l0 + c;
+            const float* o = a.offsets + e * 3;
+            dkt = qt + int(roundf(__ldg(o)));
+            if (dkt < 0 || dkt >= a.d.t) {  // "offsets leave the clip" (aggregate.cpp:108-109)
+                if (valid) latch(a.err, kErrWpsum);
+                dkt = qt;
+            }
+            const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+            const float fly = floorf(oy), flx = floorf(ox);
+            const float fy = oy - fly, fx = ox - flx;
+            const float wv = __ldg(a.weights + e);
+            d00 = wv * ((1.f - fy) * (1.f - fx));
+            d01 = wv * ((1.f - fy) * fx);
+            d10 = wv * (fy * (1.f - fx));
+            d11 = wv * (fy * fx);
+            // sample (i, j) sits between raw rows by+i, by+i+1 and cols bx+j, bx+j+1
+            dby = qy - HP + int_base(fly) + i0;
+            dbx = qx - HP + int_base(flx);
+        }
+        const int nl = min(NL, a.topl - l0);
+        for (int k = 0; k < nl; ++k) {
+            const int kt = __shfl_sync(0xffffffffu, dkt, k, NL);
+            const int by = __shfl_sync(0xffffffffu, dby, k, NL), bx = __shfl_sync(0xffffffffu, dbx, k, NL);
+            const float w00 = __shfl_sync(0xffffffffu, d00, k, NL), w01 = __shfl_sync(0xffffffffu, d01, k, NL);
+            const float w10 = __shfl_sync(0xffffffffu, d10, k, NL), w11 = __shfl_sync(0xffffffffu, d11, k, NL);
+            const u64 W00 = pk2(w00, w00), W01 = pk2(w01, w01), W10 = pk2(w10, w10), W11 = pk2(w11, w11);
+            const u64* vf = vbase + size_t(kt) * H * rowp;
+            const bool inside = by >= 0 && by + R < H && bx >= 0 && bx + P < W;
+            auto load_row = [&](int i, u64* dst) {
+                if (inside) {
+                    const u64* p0 = vf + (unsigned(by + i) * rowp + unsigned(bx) * NL);
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) dst[j] = __ldg(p0 + j * NL);
+                } else {  // reflected border taps (tensor.cpp:31-48)
+                    const unsigned r = unsigned(reflect_near(by + i, H)) * rowp;
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) dst[j] = __ldg(vf + (r + unsigned(reflect_near(bx + j, W)) * NL));
+                }
+            };
+            u64 top[P + 1], bot[P + 1];
+            load_row(0, top);
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                if (RS > 1 && P % R != 0 && i0 + i >= P) break;  // the last group's short slice
+                load_row(i + 1, bot);
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    acc[i][j] = fma2(W11, bot[j + 1], fma2(W10, bot[j], fma2(W01, top[j + 1], fma2(W00, top[j], acc[i][j]))));
+#pragma unroll
+                for (int j = 0; j <= P; ++j) top[j] = bot[j];
+            }
+        }
+    }
+    if (!valid) return;
+    u64* dst = reinterpret_cast<u64*>(patch + (size_t(row) * P + i0) * P * F) + c;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if (RS == 1 || i0 + i < P)
+#pragma unroll
+            for (int j = 0; j < P; ++j) dst[(i * P + j) * NL] = acc[i][j];
+}
+
+// S0 > 0: the stride as a compile-time constant (its divisions become multiplies); patch
+// indices are 32-bit (the launcher checks rows * ps^2 * FG < 2^31).
+template <int P, int FG, int S0>
+__global__ void __launch_bounds__(256) wpsum_combine_kernel(AggArgs a, const float* __restrict__ patch,
+                                                            float* __restrict__ out,
+                                                            int32_t* __restrict__ counts) {
+    constexpr int HP = P / 2;
+    const int H = a.d.h, W = a.d.w, st = S0 > 0 ? S0 : a.d.stride0;
+    // grid: x = pixels of one image row (FG lanes each), y = frame * H + row
+    const int idx = int(blockIdx.x) * 256 + threadIdx.x;
+    const int x = idx / FG, c = idx % FG;
+    if (x >= W) return;
+    const int y = int(blockIdx.y % unsigned(H));
+    const int ti = a.d.t0 + int(blockIdx.y / unsigned(H));
+    const int64_t gp = (int64_t(ti - a.d.t0) * H + y) * W + x;  // local output pixel
+    const float4* pv = reinterpret_cast<const float4*>(patch) + c;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cnt = 0;
+    const unsigned frame_rows = unsigned(ti - a.d.t0) * unsigned(a.d.nh * a.d.nw);
+    auto add = [&](int gy, int gx, int si, int sj) {
+        const unsigned row = frame_rows + unsigned(gy * a.d.nw + gx);
+        const float4 v = __ldg(pv + ((row * P + unsigned(si)) * P + unsigned(sj)) * FG);
+        sum.x += v.x;
+        sum.y += v.y;
+        sum.z += v.z;
+        sum.w += v.w;
+        ++cnt;
+    };
+    const AxisUnits uy = axis_units(y, st, HP, (a.d.nh - 1) * st);
+    const AxisUnits ux = axis_units(x, st, HP, (a.d.nw - 1) * st);
+    for (int iy = 0; iy < uy.n; ++iy) {
+        const int py = iy == 0 ? uy.p0 : uy.p1;
+        for (int ix = 0; ix < ux.n; ++ix) {
+            const int px = ix == 0 ? ux.p0 : ux.p1;
+            add((y - py) / st, (x - px) / st, py + HP, px + HP);
+        }
+    }
+    const int gy = owner_index(y, st, a.d.nh), gx = owner_index(x, st, a.d.nw);
+    if (abs(y - gy * st) > HP || abs(x - gx * st) > HP)
+        add(gy, gx, clampi(y - gy * st, HP) + HP, clampi(x - gx * st, HP) + HP);
+    if (cnt <= 0) {
+        latch(a.err, kErrWpsum);
+        return;
+    }
+    const float fc = float(cnt);
+    reinterpret_cast<float4*>(out + gp * a.d.f)[c] = make_float4(sum.x / fc, sum.y / fc, sum.z / fc, sum.w / fc);
+    if (c == 0 && counts) counts[gp] = cnt;
+}
+
+// The patch scratch comes from the device's stream-ordered pool (cudaMallocAsync /
+// cudaFreeAsync on the launching stream): no shared workspace, so two pipeline chunks on
+// different streams never race on it, and with the pool's release threshold raised the
+// allocation is a pool hit after the first call.
+inline void keep_pool(cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex m;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lk(m);
+    if (done.count(dev)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done.insert(dev);
+    (void)st;
+}
+
+template <int P, int NL, int RS>
+int launch_wpsum_patch(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
+    keep_pool(st);
+    const size_t bytes = size_t(a.d.rows) * P * P * a.d.f * sizeof(float);
+    void* patch = nullptr;
+    if (cudaMallocAsync(&patch, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;  // caller falls back to the one-pass gather
+    }
+    const int64_t threads = a.d.rows * RS * NL;
+    wpsum_patch_kernel<P, NL, RS><<<unsigned((threads + 255) / 256), 256, 0, st>>>(a, static_cast<float*>(patch));
+    constexpr int FG = NL / 2;
+    const dim3 cgrid(unsigned((a.d.w * FG + 255) / 256), unsigned(a.d.nt * a.d.h));
+    const float* pp = static_cast<const float*>(patch);
+    if (a.d.stride0 == 4)
+        wpsum_combine_kernel<P, FG, 4><<<cgrid, 256, 0, st>>>(a, pp, out, counts);
+    else
+        wpsum_combine_kernel<P, FG, 0><<<cgrid, 256, 0, st>>>(a, pp, out, counts);
+    cudaFreeAsync(patch, st);
+    return 2;
+}
+
+int wpsum_patch_rs() {
+    static const int rs = [] {
+        const char* e = std::getenv("SNLS_WPSUM_RS");  // A/B: 0 = one-pass gather, 1 / 2 / 4 slices
+        return e ? std::atoi(e) : 4;
+    }();
+    return rs;
+}
+
+int launch_wpsum_patch_any(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
+    const int rs = wpsum_patch_rs();
+    if (rs <= 0 || int64_t(a.d.nt) * a.d.h > 65535) return 0;  // (combine grid.y)
+    if (a.d.rows * a.ps * a.ps * (a.d.f / 4) >= (int64_t(1) << 31)) return 0;  // 32-bit patch index
+    if (a.ps == 7 && a.d.f == 64)
+        return rs == 4   ? launch_wpsum_patch<7, 32, 4>(a, out, counts, st)
+               : rs == 2 ? launch_wpsum_patch<7, 32, 2>(a, out, counts, st)
+                         : launch_wpsum_patch<7, 32, 1>(a, out, counts, st);
+    if (a.ps == 7 && a.d.f == 32)
+        return rs == 4   ? launch_wpsum_patch<7, 16, 4>(a, out, counts, st)
+               : rs == 2 ? launch_wpsum_patch<7, 16, 2>(a, out, counts, st)
+                         : launch_wpsum_patch<7, 16, 1>(a, out, counts, st);
+    if (a.ps == 5 && a.d.f == 64) return launch_wpsum_patch<5, 32, 1>(a, out, counts, st);
+    if (a.ps == 5 && a.d.f == 32) return launch_wpsum_patch<5, 16, 1>(a, out, counts, st);
+    return 0;
+}
+
 int launch_wpsum_query_any(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     if (a.d.f % 4 != 0) return 0;
     const int FG = a.d.f / 4;
@@ -882,6 +1103,8 @@ int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* we
 
 int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     if (int n = launch_wpsum_query_any(a, out, counts, st)) return n;
+    if (int64_t(a.d.t) * a.d.h * a.d.w < (int64_t(1) << 31))
+        if (int n = launch_wpsum_patch_any(a, out, counts, st)) return n;
     if (int n = launch_tiled_agg_any(a, out, counts, 0, st)) return n;
     const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {

@@ -931,6 +931,9 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
 #define SNLS_WBWD_GSSM 1
 #endif
 constexpr bool kGsSm = SNLS_WBWD_GSSM != 0;
+#ifndef SNLS_WBWD_ROLL
+#define SNLS_WBWD_ROLL 1
+#endif
 
 // FT > 0: compile-time channel count; raw blocks inside the frame use immediate column
 // offsets from one row base (no reflection / per-element address math), as search_bwd_rows.
@@ -1033,7 +1036,10 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
                 rb[j] = act ? __ldg(vb + rob + colo(j)) : 0.f;
                 ka[j] = 0.f;
             }
-#pragma unroll
+            // rolled for wide patches: unrolled, the two block bodies of ps 7 are ~10k SASS
+            // instructions and the warps wait on instruction fetch
+            constexpr bool kRoll = SNLS_WBWD_ROLL && kGsSm && P > 3;
+#pragma unroll(kRoll ? 1 : P)
             for (int i = 0; i < P; ++i) {
                 // raw row i+2 is loaded one row ahead (its latency overlaps row i's arithmetic)
                 float rn[P + 1];

@@ -153,16 +153,24 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 // FT > 0: the channel count as a compile-time constant; entries whose raw block lies inside
 // the frame then address it as row base + j * FT (immediate offsets: no reflection, no
 // per-element address arithmetic -- most of this kernel's integer work); FT = 0 any F.
-template <int P, bool DET, bool CORR, int FT = 0>
+// MET: 0 = runtime metric, 1 + snls_metric = compile-time (drops the other metric's selects
+// and, for ip, the l2-only CORR sums).  The patch-row loop is rolled (ROLL): fully unrolled,
+// the two block bodies of a ps 7 instantiation took ~12k SASS instructions and the warps
+// stalled on instruction fetch (no_instructions 27%, profiles/r02f_ncu_c3.txt).
+#ifndef SNLS_BWD_ROLL
+#define SNLS_BWD_ROLL 1
+#endif
+template <int P, bool DET, bool CORR, int FT = 0, int MET = 0>
 __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const float* __restrict__ grad,
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
                                                           const float* __restrict__ k, Dims d,
-                                                          int topl, int metric,
+                                                          int topl, int metric_rt,
                                                           Sink sinkq, Sink sinkk,
                                                           double* __restrict__ gyx,
                                                           const double* __restrict__ centers) {
     constexpr int HP = P / 2;
+    const int metric = MET ? MET - 1 : metric_rt;
     const double scq = DET ? *sinkq.scale : 0.0, sck = DET ? *sinkk.scale : 0.0;
     const int slices = (d.f + 31) / 32;
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -260,7 +268,8 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
                 rb[j] = act ? __ldg(kb + rob + colo(j)) : 0.f;
                 ka[j] = 0.f;
             }
-#pragma unroll
+            constexpr bool kRoll = SNLS_BWD_ROLL && kDqSm && P > 3;
+#pragma unroll(kRoll ? 1 : P)
             for (int py = 0; py < P; ++py) {
                 const size_t ron = rowo(py + 2);
 #pragma unroll
@@ -371,13 +380,14 @@ void launch_rows(const float* grad, const float* offsets, const float* q, const 
     };
     // compile-time channel counts of the BASELINE shapes (fast interior addressing)
     const int ft = DET ? 0 : (d.f == 64 ? 64 : (d.f == 32 ? 32 : 0));
+    const bool ip = metric == SNLS_METRIC_IP;
     if (centers) {
-        if (ft == 64) go(search_bwd_rows<P, DET, true, DET ? 0 : 64>);
-        else if (ft == 32) go(search_bwd_rows<P, DET, true, DET ? 0 : 32>);
+        if (ft == 64) ip ? go(search_bwd_rows<P, DET, true, DET ? 0 : 64, 1>) : go(search_bwd_rows<P, DET, true, DET ? 0 : 64, 2>);
+        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, true, DET ? 0 : 32, 1>) : go(search_bwd_rows<P, DET, true, DET ? 0 : 32, 2>);
         else go(search_bwd_rows<P, DET, true, 0>);
     } else {
-        if (ft == 64) go(search_bwd_rows<P, DET, false, DET ? 0 : 64>);
-        else if (ft == 32) go(search_bwd_rows<P, DET, false, DET ? 0 : 32>);
+        if (ft == 64) ip ? go(search_bwd_rows<P, DET, false, DET ? 0 : 64, 1>) : go(search_bwd_rows<P, DET, false, DET ? 0 : 64, 2>);
+        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, false, DET ? 0 : 32, 1>) : go(search_bwd_rows<P, DET, false, DET ? 0 : 32, 2>);
         else go(search_bwd_rows<P, DET, false, 0>);
     }
 }

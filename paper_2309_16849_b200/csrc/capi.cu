@@ -746,6 +746,7 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
         return fail(SNLS_EARG, "wpsum_backward: null tensor");
     if (t0 < 0 || t1 > dims.t || t0 >= t1)
         return fail(SNLS_EARG, "wpsum_backward: empty or invalid frame range");
+    if (int rc = check_aligned("wpsum_backward", {grad_out, v, weights, offsets, dv, dw})) return rc;
     DeviceGuard g(ctx->device);
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     cudaMemsetAsync(dv, 0, size_t(dims.t) * dims.h * dims.w * dims.f * sizeof(float), ctx->stream);

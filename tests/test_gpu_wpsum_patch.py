@@ -45,3 +45,21 @@ def test_patch_wpsum_vs_oracle(port, ps, f, s0):
     o2, c2 = S.wpsum(dev(v), dev(wts[nq:3 * nq]), dev(offs[nq:3 * nq]), scfg(cfg), frames=(1, 3))
     assert np.array_equal(host(o2), host(out)[1:3])
     assert np.array_equal(host(c2), host(cnt)[1:3])
+
+
+@pytest.mark.parametrize("ps,f,s0", CASES, ids=[f"p{p}f{f}s{s}" for p, f, s in CASES])
+def test_pairs_wpsum_backward_vs_oracle(port, ps, f, s0):
+    """wpsum_backward's channel-pair kernel (wpsum_bwd_pairs: ps 5/7 at F 32/64) against the
+    oracle (aggregate.cpp:351-460): dV and dW, borders and cell completion in play."""
+    S = snls_mod()
+    t, h, w = 4, 29, 26
+    cfg = Cfg(ws=5, wt=1, ps=ps, stride0=s0, topl=6, metric="l2", softmax_scale=1.0)
+    v = video(port, t, h, w, f, 60 + ps + f + s0)
+    wts, offs = _selection(t, h, w, cfg, 11 * ps + s0)
+    _, cnt = S.wpsum(dev(v), dev(wts), dev(offs), scfg(cfg))
+    go = video(port, t, h, w, f, 90 + s0)
+    dv, dw = S.wpsum_backward(dev(go), cnt, dev(v), dev(wts), dev(offs), scfg(cfg))
+    wdv, wdw = port.wpsum_bwd(go, host(cnt), v, wts, offs, cfg, deterministic=False)
+    edv, edw = max_rel(host(dv), wdv), max_rel(host(dw), wdw)
+    print(f"[pairs wpsum bwd p{ps} f{f} s{s0}] dV {edv:.2e} dW {edw:.2e}")
+    assert edv <= REL_TOL and edw <= REL_TOL

@@ -795,6 +795,14 @@ int wpsum_patch_rs() {
     return rs;
 }
 
+int wpsum_patch3() {
+    static const int on = [] {
+        const char* e = std::getenv("SNLS_WPSUM_PATCH3");
+        return e ? std::atoi(e) : 0;
+    }();
+    return on;
+}
+
 int launch_wpsum_patch_any(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
     const int rs = wpsum_patch_rs();
     if (rs <= 0 || int64_t(a.d.nt) * a.d.h > 65535) return 0;  // (combine grid.y)
@@ -807,6 +815,10 @@ int launch_wpsum_patch_any(const AggArgs& a, float* out, int32_t* counts, cudaSt
         return rs == 4   ? launch_wpsum_patch<7, 16, 4>(a, out, counts, st)
                : rs == 2 ? launch_wpsum_patch<7, 16, 2>(a, out, counts, st)
                          : launch_wpsum_patch<7, 16, 1>(a, out, counts, st);
+    if (a.ps == 3 && wpsum_patch3()) {  // A/B: the query-centric kernel is the default at ps 3
+        if (a.d.f == 32) return launch_wpsum_patch<3, 16, 1>(a, out, counts, st);
+        if (a.d.f == 64) return launch_wpsum_patch<3, 32, 1>(a, out, counts, st);
+    }
     if (a.ps == 5 && a.d.f == 64) return launch_wpsum_patch<5, 32, 1>(a, out, counts, st);
     if (a.ps == 5 && a.d.f == 32) return launch_wpsum_patch<5, 16, 1>(a, out, counts, st);
     return 0;
@@ -1281,9 +1293,9 @@ int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* we
 }
 
 int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st) {
-    if (int n = launch_wpsum_query_any(a, out, counts, st)) return n;
     if (int64_t(a.d.t) * a.d.h * a.d.w < (int64_t(1) << 31))
         if (int n = launch_wpsum_patch_any(a, out, counts, st)) return n;
+    if (int n = launch_wpsum_query_any(a, out, counts, st)) return n;
     if (int n = launch_tiled_agg_any(a, out, counts, 0, st)) return n;
     const int64_t npix = int64_t(a.d.nt) * a.d.h * a.d.w;
     if (a.d.f % 4 == 0) {

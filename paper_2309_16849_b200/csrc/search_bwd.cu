@@ -16,6 +16,12 @@
 #ifndef SNLS_BWD_DQSM
 #define SNLS_BWD_DQSM 1
 #endif
+#ifndef SNLS_BWD_ACT_CT
+#define SNLS_BWD_ACT_CT 0
+#endif
+#ifndef SNLS_BWD_MINB
+#define SNLS_BWD_MINB 4
+#endif
 #ifndef SNLS_BWD_FORCE_ENTRIES
 #define SNLS_BWD_FORCE_ENTRIES 0
 #endif
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 #define SNLS_BWD_ROLL 1
 #endif
 template <int P, bool DET, bool CORR, int FT = 0, int MET = 0>
-__global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const float* __restrict__ grad,
+__global__ void __launch_bounds__(128, SNLS_BWD_MINB) search_bwd_rows(const float* __restrict__ grad,
                                                           const float* __restrict__ offsets,
                                                           const float* __restrict__ q,
                                                           const float* __restrict__ k, Dims d,
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(128, kDqSm ? 4 : 3) search_bwd_rows(const floa
     if (wid >= d.rows * slices) return;  // warp-uniform
     const int64_t row = wid / slices;
     const int c = int(wid % slices) * 32 + lane;
-    const bool act = c < d.f;
+    const bool act = (SNLS_BWD_ACT_CT && FT > 0 && FT % 32 == 0) || c < d.f;
     const int cc = act ? c : 0;
     // dynamic shared memory: [4 warps][P*P][32] query patch, then (kDqSm) the dQ partials
     extern __shared__ float s_bwd[];

@@ -26,6 +26,8 @@ struct snls_ctx {
     int search_kernel = 0;
     int last_path = -1;
     int band = -1;  // temporally blocked search raster: -1 auto (search_band), 0 off, > 0 rows
+    cudaStream_t aux = nullptr;  // snls_train_bwd: the wpsum backward beside the search backward
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace snls_capi {
@@ -258,6 +260,12 @@ int snls_ctx_destroy(snls_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->err) cudaFree(ctx->err);
     if (ctx->work) cudaFree(ctx->work);
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
+        cudaEventDestroy(ctx->fork);
+        cudaEventDestroy(ctx->join);
+    }
     delete ctx;
     return SNLS_OK;
 }
@@ -832,17 +840,88 @@ int snls_gaussian_noise_f32(uint64_t seed, double sigma, int64_t n, const float*
     return SNLS_OK;
 }
 
+static int train_bwd_concurrent() {
+    static const int on = [] {
+        const char* e = std::getenv("SNLS_TRAIN_BWD_CONCURRENT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on;
+}
+
 int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const float* grad_sims,
                    const float* grad_out, const int32_t* counts, const float* offsets,
                    const float* chains, const double* centers, const double* chains64,
                    const float* q, const float* k, const float* v, const float* weights, float* dq,
                    float* dk, float* dv, float* dweights, float* dfflow, float* dbflow, int flags) {
-    // the two operators one after the other (a single fused kernel for v == k was measured
-    // slower: 168 registers and three shared-memory patches per warp, 12 warps/SM -- c3
-    // backward 0.80 vs 0.585 ms, profiles/r01_plans.txt)
-    if (int rc = snls_wpsum_bwd(ctx, cfg, dims, grad_out, counts, v, weights, offsets, dv, dweights)) return rc;
-    return snls_search_bwd_ex(ctx, cfg, dims, 0, dims.t, grad_sims, centers ? nullptr : offsets,
-                              centers ? nullptr : chains, centers, chains64, q, k, dq, dk, dfflow, dbflow, flags);
+    // the two operators (a single fused kernel for v == k was measured slower: 168 registers
+    // and three shared-memory patches per warp, 12 warps/SM -- c3 backward 0.80 vs 0.585 ms,
+    // profiles/r01_plans.txt).  Their outputs are disjoint, so the wpsum backward (bound by
+    // its dV reductions through L2) runs on a second stream beside the search backward
+    // (issue-bound); with aliased outputs they run one after the other.
+    auto search = [&] {
+        return snls_search_bwd_ex(ctx, cfg, dims, 0, dims.t, grad_sims, centers ? nullptr : offsets,
+                                  centers ? nullptr : chains, centers, chains64, q, k, dq, dk, dfflow,
+                                  dbflow, flags);
+    };
+    const bool disjoint = dv != dk && dv != dq && (void*)dweights != (void*)dk && (void*)dweights != (void*)dq;
+    if (disjoint && flags == 0 && ctx && cfg && train_bwd_interleavable(cfg->ps, dims.f)) {
+        // one interleaved phase-1 launch (search_bwd.cu train_bwd_interleaved); the checks of
+        // both operators first (snls_wpsum_bwd_frames, snls_search_bwd_ex)
+        if (int rc = check_ctx(ctx)) return rc;
+        if (int rc = validate(cfg)) return rc;
+        if (int rc = check_dims(dims)) return rc;
+        if (!grad_sims || !q || !k || !dq || !dk || !dfflow || !dbflow || !grad_out || !counts || !v ||
+            !weights || !offsets || !dv || !dweights)
+            return fail(SNLS_EARG, "train_backward: null tensor");
+        if (cfg->wt > 1 && (centers ? chains64 == nullptr : chains == nullptr))
+            return fail(SNLS_EARG, "shifted_nls_backward: the tape needs chains when wt > 1");
+        if (int rc = check_aligned("train_backward", {q, k, v, dq, dk, grad_out, weights, offsets, dv, dweights}))
+            return rc;
+        DeviceGuard g(ctx->device);
+        const Dims d = make_dims(dims, cfg->stride0);
+        const size_t nv = size_t(dims.t) * dims.h * dims.w;
+        cudaMemsetAsync(dq, 0, nv * dims.f * sizeof(float), ctx->stream);
+        cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
+        cudaMemsetAsync(dv, 0, nv * dims.f * sizeof(float), ctx->stream);
+        cudaMemsetAsync(dweights, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
+        const size_t scratch = (size_t(d.rows) * cfg->topl * 2 + nv * 4) * sizeof(double);
+        if (int rc = ensure_work(ctx, scratch)) return rc;
+        cudaMemsetAsync(ctx->work, 0, scratch, ctx->stream);
+        const WpsumBwdArgs wp{AggArgs{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err, cfg->wt}, grad_out,
+                              counts, dv, dweights};
+        const int n = launch_train_bwd_interleaved(grad_sims, centers ? nullptr : offsets, centers ? nullptr : chains,
+                                                   centers, chains64, q, k, d, cfg->wt, cfg->ps, cfg->topl,
+                                                   cfg->metric, dq, dk, dfflow, dbflow,
+                                                   static_cast<double*>(ctx->work), wp, ctx->stream);
+        return after_launch(ctx, n, "snls_train_bwd");
+    }
+    if (!disjoint || !train_bwd_concurrent())
+        {
+            if (int rc = snls_wpsum_bwd(ctx, cfg, dims, grad_out, counts, v, weights, offsets, dv, dweights)) return rc;
+            return search();
+        }
+    if (int rc = check_ctx(ctx)) return rc;
+    DeviceGuard g(ctx->device);
+    if (!ctx->aux) {
+        static const int prio = [] {  // A/B: stream priority of the wpsum backward
+            const char* e = std::getenv("SNLS_TRAIN_BWD_PRIO");
+            return e ? std::atoi(e) : 0;
+        }();
+        cudaError_t e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "snls_train_bwd: stream");
+    }
+    cudaStream_t main = ctx->stream;
+    cudaEventRecord(ctx->fork, main);
+    cudaStreamWaitEvent(ctx->aux, ctx->fork, 0);
+    ctx->stream = ctx->aux;
+    int rc = snls_wpsum_bwd(ctx, cfg, dims, grad_out, counts, v, weights, offsets, dv, dweights);
+    ctx->stream = main;
+    cudaEventRecord(ctx->join, ctx->aux);
+    const int rs = rc == SNLS_OK ? search() : rc;
+    cudaStreamWaitEvent(main, ctx->join, 0);  // (also on failure: nothing outlives the call)
+    return rs;
 }
 
 }  // extern "C"

@@ -93,6 +93,23 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
                            const double* centers, const double* chains64, const float* q,
                            const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
                            float* dk, float* dff, float* dbf, double* gyx, cudaStream_t st);
+// The training backward's phase 1 as one interleaved launch (search backward + wpsum backward
+// blocks side by side, search_bwd.cu train_bwd_interleaved), then the search backward's flow
+// route.  `wp`: the wpsum backward's arguments (dv, dw zeroed by the caller).  0 when the
+// shape has no interleaved instantiation (ps 5 / 7 with F 32 / 64).
+struct WpsumBwdArgs {
+    AggArgs a;
+    const float* go;
+    const int32_t* counts;
+    float* dv;
+    float* dw;
+};
+bool train_bwd_interleavable(int ps, int f);
+int launch_train_bwd_interleaved(const float* grad, const float* offsets, const float* chains,
+                                 const double* centers, const double* chains64, const float* q,
+                                 const float* k, Dims d, int wt, int ps, int topl, int metric,
+                                 float* dq, float* dk, float* dff, float* dbf, double* gyx,
+                                 const WpsumBwdArgs& wp, cudaStream_t st);
 int launch_search_bwd_det(const float* grad, const float* offsets, const float* chains,
                           const double* centers, const double* chains64, const float* q,
                           const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,

@@ -8,10 +8,13 @@
 // Phase 2: one thread per entry routes (gy, gx) back through the composition chain
 // (search.cpp:584-666): dt >= 0 into dFflow, dt < 0 into dBflow, v <- (I + J)^T v per link.
 // Entries with a zero upstream gradient are skipped (search.cpp:692).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "packed.cuh"
+#include "wpsum_bwd_pairs.cuh"
 
 #ifndef SNLS_BWD_DQSM
 #define SNLS_BWD_DQSM 1
@@ -167,19 +170,20 @@ __global__ void __launch_bounds__(256) search_bwd_entries(const float* __restric
 #define SNLS_BWD_ROLL 1
 #endif
 template <int P, bool DET, bool CORR, int FT = 0, int MET = 0>
-__global__ void __launch_bounds__(128, SNLS_BWD_MINB) search_bwd_rows(const float* __restrict__ grad,
-                                                          const float* __restrict__ offsets,
-                                                          const float* __restrict__ q,
-                                                          const float* __restrict__ k, Dims d,
-                                                          int topl, int metric_rt,
-                                                          Sink sinkq, Sink sinkk,
-                                                          double* __restrict__ gyx,
-                                                          const double* __restrict__ centers) {
+__device__ __forceinline__ void search_bwd_rows_body(const float* __restrict__ grad,
+                                                     const float* __restrict__ offsets,
+                                                     const float* __restrict__ q,
+                                                     const float* __restrict__ k, Dims d,
+                                                     int topl, int metric_rt,
+                                                     Sink sinkq, Sink sinkk,
+                                                     double* __restrict__ gyx,
+                                                     const double* __restrict__ centers,
+                                                     unsigned bid, float* s_bwd) {
     constexpr int HP = P / 2;
     const int metric = MET ? MET - 1 : metric_rt;
     const double scq = DET ? *sinkq.scale : 0.0, sck = DET ? *sinkk.scale : 0.0;
     const int slices = (d.f + 31) / 32;
-    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = (int64_t(bid) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= d.rows * slices) return;  // warp-uniform
     const int64_t row = wid / slices;
@@ -187,7 +191,6 @@ __global__ void __launch_bounds__(128, SNLS_BWD_MINB) search_bwd_rows(const floa
     const bool act = (SNLS_BWD_ACT_CT && FT > 0 && FT % 32 == 0) || c < d.f;
     const int cc = act ? c : 0;
     // dynamic shared memory: [4 warps][P*P][32] query patch, then (kDqSm) the dQ partials
-    extern __shared__ float s_bwd[];
     float* sq = s_bwd + (threadIdx.x >> 5) * (P * P * 32) + lane;
     float* sdq = sq + 4 * P * P * 32;
     int qt, qy, qx;
@@ -371,6 +374,48 @@ sy = fma(double(gk), double(dkv_dy), sy);
                 put<DET>(sinkq.f, sinkq.i, scq, dqb + size_t(qrow[py] + qcol[px]) * F,
                          kDqSm ? sdq[(py * P + px) * 32] : dqa[py][px]);
     }
+}
+
+template <int P, bool DET, bool CORR, int FT = 0, int MET = 0>
+__global__ void __launch_bounds__(128, SNLS_BWD_MINB) search_bwd_rows(const float* __restrict__ grad,
+                                                          const float* __restrict__ offsets,
+                                                          const float* __restrict__ q,
+                                                          const float* __restrict__ k, Dims d,
+                                                          int topl, int metric_rt,
+                                                          Sink sinkq, Sink sinkk,
+                                                          double* __restrict__ gyx,
+                                                          const double* __restrict__ centers) {
+    extern __shared__ float s_bwd[];
+    search_bwd_rows_body<P, DET, CORR, FT, MET>(grad, offsets, q, k, d, topl, metric_rt, sinkq, sinkk,
+                                                gyx, centers, blockIdx.x, s_bwd);
+}
+
+// The training backward's two phase-1 operators in ONE launch, their blocks interleaved
+// (even: a search-backward block, odd: a wpsum-backward block, then the longer one's rest):
+// every SM runs both at once -- the search backward is issue-bound, the wpsum backward waits
+// on its dV reductions through L2 -- instead of one after the other (or overlapping only at
+// the tail when launched on two streams).  Same bodies, same results.
+template <int P, bool CORR, int FT, int MET, int NL, int LS>
+__global__ void __launch_bounds__(128, SNLS_BWD_MINB) train_bwd_interleaved(
+    const float* __restrict__ grad, const float* __restrict__ offsets, const float* __restrict__ q,
+    const float* __restrict__ k, Dims d, int topl, Sink sinkq, Sink sinkk, double* __restrict__ gyx,
+    const double* __restrict__ centers, WpsumBwdArgs w, unsigned n_search, unsigned n_wpsum) {
+    extern __shared__ float s_bwd[];
+    const unsigned m = min(n_search, n_wpsum), b = blockIdx.x;
+    bool wp;
+    unsigned idx;
+    if (b < 2 * m) {
+        wp = b & 1u;
+        idx = b >> 1;
+    } else {
+        wp = n_wpsum > n_search;
+        idx = b - m;
+    }
+    if (wp)
+        wpsum_bwd_pairs_body<P, NL, LS>(w.a, w.go, w.counts, w.dv, w.dw, idx, reinterpret_cast<u64*>(s_bwd));
+    else
+        search_bwd_rows_body<P, false, CORR, FT, MET>(grad, offsets, q, k, d, topl, MET - 1, sinkq, sinkk,
+                                                      gyx, centers, idx, s_bwd);
 }
 
 template <int P, bool DET>
@@ -571,6 +616,65 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
     double* dbf64 = dff64 + nfl;
     const Sink sq{dq, nullptr, nullptr}, sk{dk, nullptr, nullptr};
     launch_phase1<false>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, st);
+    const int64_t ne = d.rows * topl;
+    search_bwd_route<0><<<unsigned((ne + 255) / 256), 256, 0, st>>>(
+        grad, offsets, chains, d, wt, topl, gyx, 1, dff64, dbf64, nullptr, nullptr, nullptr, nullptr,
+        centers, chains64);
+    narrow_kernel<<<unsigned(std::min<int64_t>((nfl + 255) / 256, 4096)), 256, 0, st>>>(dff64, dbf64, dff,
+                                                                                       dbf, nfl);
+    return 3;
+}
+
+#ifndef SNLS_WBWD_LSPLIT_IL
+#define SNLS_WBWD_LSPLIT_IL 2
+#endif
+bool train_bwd_interleavable(int ps, int f) {
+    static const int on = [] {
+        const char* e = std::getenv("SNLS_TRAIN_BWD_INTERLEAVE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on && kDqSm && (ps == 5 || ps == 7) && (f == 32 || f == 64);
+}
+
+namespace {
+template <int P, int FT>
+void launch_interleaved_p(const float* grad, const float* offsets, const double* centers, const float* q,
+                          const float* k, Dims d, int topl, int metric, Sink sq, Sink sk, double* gyx,
+                          const WpsumBwdArgs& wp, cudaStream_t st) {
+    constexpr int NL = FT / 2, LS = SNLS_WBWD_LSPLIT_IL;
+    const unsigned n_search = unsigned((d.rows * (FT / 32) + 3) / 4);
+    const unsigned n_wpsum = unsigned((wp.a.d.rows * LS + 128 / NL - 1) / (128 / NL));
+    const size_t smem = size_t(4) * P * P * 32 * sizeof(float) * 2;  // = the wpsum body's [128/NL][P*P][NL] u64
+    static_assert(size_t(128 / NL) * P * P * NL * sizeof(u64) <= size_t(4) * P * P * 32 * sizeof(float) * 2, "smem");
+    auto go = [&](auto kern) {
+        ensure_smem(kern, smem);
+        kern<<<n_search + n_wpsum, 128, smem, st>>>(grad, offsets, q, k, d, topl, sq, sk, gyx, centers, wp,
+                                                    n_search, n_wpsum);
+    };
+    const bool ip = metric == SNLS_METRIC_IP;
+    if (centers)
+        ip ? go(train_bwd_interleaved<P, true, FT, 1, NL, LS>) : go(train_bwd_interleaved<P, true, FT, 2, NL, LS>);
+    else
+        ip ? go(train_bwd_interleaved<P, false, FT, 1, NL, LS>) : go(train_bwd_interleaved<P, false, FT, 2, NL, LS>);
+}
+}  // namespace
+
+int launch_train_bwd_interleaved(const float* grad, const float* offsets, const float* chains,
+                                 const double* centers, const double* chains64, const float* q,
+                                 const float* k, Dims d, int wt, int ps, int topl, int metric,
+                                 float* dq, float* dk, float* dff, float* dbf, double* gyx,
+                                 const WpsumBwdArgs& wp, cudaStream_t st) {
+    if (!train_bwd_interleavable(ps, d.f)) return 0;
+    const Sink sq{dq, nullptr, nullptr}, sk{dk, nullptr, nullptr};
+    if (ps == 7)
+        d.f == 64 ? launch_interleaved_p<7, 64>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
+                  : launch_interleaved_p<7, 32>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
+    else
+        d.f == 64 ? launch_interleaved_p<5, 64>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
+                  : launch_interleaved_p<5, 32>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
+    double* dff64 = gyx + size_t(d.rows) * topl * 2;
+    const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
+    double* dbf64 = dff64 + nfl;
     const int64_t ne = d.rows * topl;
     search_bwd_route<0><<<unsigned((ne + 255) / 256), 256, 0, st>>>(
         grad, offsets, chains, d, wt, topl, gyx, 1, dff64, dbf64, nullptr, nullptr, nullptr, nullptr,

@@ -63,3 +63,38 @@ def test_pairs_wpsum_backward_vs_oracle(port, ps, f, s0):
     edv, edw = max_rel(host(dv), wdv), max_rel(host(dw), wdw)
     print(f"[pairs wpsum bwd p{ps} f{f} s{s0}] dV {edv:.2e} dW {edw:.2e}")
     assert edv <= REL_TOL and edw <= REL_TOL
+
+
+TRAIN = [(5, 32, 3, "l2"), (7, 32, 4, "ip"), (5, 64, 4, "ip"), (7, 64, 5, "l2")]
+
+
+@pytest.mark.parametrize("ps,f,s0,metric", TRAIN, ids=[f"p{p}f{f}s{s}{m}" for p, f, s, m in TRAIN])
+def test_train_backward_interleaved_vs_separate_and_oracle(port, ps, f, s0, metric):
+    """snls_train_bwd's interleaved launch (search + wpsum backward blocks side by side,
+    search_bwd.cu train_bwd_interleaved) equals the two operators called separately and the
+    oracle's backward operators (search.cpp:499-711, aggregate.cpp:351-460)."""
+    from tests.helpers import flow
+
+    S = snls_mod()
+    t, h, w = 4, 21, 19
+    cfg = Cfg(ws=5, wt=1, ps=ps, stride0=s0, topl=5, metric=metric, softmax_scale=0.05)
+    q, k, v = (video(port, t, h, w, f, 300 + i + ps + f) for i in range(3))
+    ff, bf = flow(port, t, h, w, 310 + ps, 1.5), flow(port, t, h, w, 311 + ps, 1.5)
+    r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), want_weights=True)
+    cen, ch = S.search_tape64(r, dev(ff), dev(bf))
+    rows, L = r.sims.shape
+    g = f32(port.uniform(320, -1, 1, rows * L).reshape(rows, L))
+    _, cnt = S.wpsum(dev(v), r.weights, r.offsets, scfg(cfg))
+    go = video(port, t, h, w, f, 330)
+    got = [host(x) for x in S.train_backward(dev(g), dev(go), cnt, r, dev(q), dev(k), dev(v), tape64=(cen, ch))]
+    dq, dk, dff, dbf = [host(x) for x in S.shifted_nls_backward(dev(g), r, dev(q), dev(k), tape64=(cen, ch))]
+    dv, dw = [host(x) for x in S.wpsum_backward(dev(go), cnt, dev(v), r.weights, r.offsets, scfg(cfg))]
+    for a, b, name in zip(got, (dq, dk, dv, dff, dbf, dw), ("dq", "dk", "dv", "dff", "dbf", "dw")):
+        assert max_rel(a, b) <= REL_TOL, (name, max_rel(a, b))
+    sb = port.search_bwd(q, k, cfg, cen.cpu().numpy(), None if ch is None else ch.cpu().numpy(), g)
+    wdv, wdw = port.wpsum_bwd(go, host(cnt), v, host(r.weights), host(r.offsets), cfg)
+    for a, b, name in zip(got, (sb["dq"], sb["dk"], wdv, sb["dfflow"], sb["dbflow"], wdw),
+                          ("dq", "dk", "dv", "dff", "dbf", "dw")):
+        err = max_rel(a, b)
+        print(f"[train bwd p{ps} f{f} s{s0} {metric}] {name} {err:.2e}")
+        assert err <= REL_TOL, (name, err)

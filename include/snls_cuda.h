@@ -279,6 +279,13 @@ int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
 int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
                           const float* grad_out, const int32_t* counts, const float* v,
                           const float* weights, const float* offsets, float* dv, float* dweights);
+/* wpsum_backward with flags: SNLS_BWD_DETERMINISTIC = the reference's default
+ * ExecPolicy::deterministic (aggregate.cpp:439-450, dV gathered in a fixed order): here int64
+ * fixed-point accumulation, bitwise identical run to run.  0 = atomics (aggregate.cpp:451-458). */
+int snls_wpsum_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                      const float* grad_out, const int32_t* counts, const float* v,
+                      const float* weights, const float* offsets, float* dv, float* dweights,
+                      int flags);
 
 /* The whole backward of search -> softmax weights -> wpsum in one call: wpsum_backward (dv,
  * dweights from grad_out / counts) then shifted_nls_backward (dq, dk, dfflow, dbflow; tape =

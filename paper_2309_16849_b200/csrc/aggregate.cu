@@ -8,6 +8,7 @@
 // C-vectorised (float4) reads of V.  The backward scatters through 4 bilinear taps, so it
 // uses atomics (the reference's non-deterministic mode, aggregate.cpp:451-458).
 #include <cstdlib>
+#include <functional>
 #include <mutex>
 #include <set>
 #include <type_traits>
@@ -15,6 +16,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "packed.cuh"
+#include "fixed_point.cuh"
 #include "wpsum_bwd_pairs.cuh"
 
 namespace snls_gpu {
@@ -860,11 +862,11 @@ __global__ void softmax_kernel(int64_t rows, int l, float beta, const float* __r
 
 // wpsum backward (aggregate.cpp:351-408): one thread per (row, neighbour, channel group);
 // dW partial sums reduced with one atomic per thread, dV scattered through the 4 taps.
-template <int VEC>
+template <int VEC, bool DET = false>
 __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* __restrict__ go,
                                                         const int32_t* __restrict__ counts,
                                                         float* __restrict__ dv,
-                                                        float* __restrict__ dw) {
+                                                        float* __restrict__ dw, WbwdFixed fxp) {
     const int groups = a.d.f / VEC;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= a.d.rows * a.topl * groups) return;
@@ -916,13 +918,22 @@ __global__ void __launch_bounds__(256) wpsum_bwd_kernel(AggArgs a, const float* 
                                        __ldg(a.v + i10 + j), __ldg(a.v + i11 + j));
             dw_acc = fmaf(g, sample, dw_acc);
             const float gv = g * wv;
-            atomicAdd(dv + i00 + j, gv * t.w00);
-            atomicAdd(dv + i01 + j, gv * t.w01);
-            atomicAdd(dv + i10 + j, gv * t.w10);
-            atomicAdd(dv + i11 + j, gv * t.w11);
+            if constexpr (DET) {
+                const double sv = fxp.scale[0];
+                fixed_add(fxp.dvi + i00 + j, gv * t.w00, sv);
+                fixed_add(fxp.dvi + i01 + j, gv * t.w01, sv);
+                fixed_add(fxp.dvi + i10 + j, gv * t.w10, sv);
+                fixed_add(fxp.dvi + i11 + j, gv * t.w11, sv);
+            } else {
+                atomicAdd(dv + i00 + j, gv * t.w00);
+                atomicAdd(dv + i01 + j, gv * t.w01);
+                atomicAdd(dv + i10 + j, gv * t.w10);
+                atomicAdd(dv + i11 + j, gv * t.w11);
+            }
         }
     }
-    atomicAdd(dw + e, dw_acc);
+    if constexpr (DET) fixed_add(fxp.dwi + e, dw_acc, fxp.scale[1]);
+    else atomicAdd(dw + e, dw_acc);
 }
 
 // Row-centric wpsum backward (aggregate.cpp:351-460): one warp per (query row, 32-channel
@@ -943,10 +954,11 @@ constexpr bool kGsSm = SNLS_WBWD_GSSM != 0;
 
 // FT > 0: compile-time channel count; raw blocks inside the frame use immediate column
 // offsets from one row base (no reflection / per-element address math), as search_bwd_rows.
-template <int P, int FT = 0>
+template <int P, int FT = 0, bool DET = false>
 __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, const float* __restrict__ go,
                                                          const int32_t* __restrict__ counts,
-                                                         float* __restrict__ dv, float* __restrict__ dw) {
+                                                         float* __restrict__ dv, float* __restrict__ dw,
+                                                         WbwdFixed fxp) {
     constexpr int HP = P / 2;
     const int slices = (a.d.f + 31) / 32;
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1020,7 +1032,12 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
         const float wv = __ldg(a.weights + e);
         const int by = qy - HP + int_base(fly), bx = qx - HP + int_base(flx);
         const float* __restrict__ vb = a.v + size_t(kt) * frameF + cc;
-        float* dvb = dv + size_t(kt) * frameF + cc;
+        const size_t dvo = size_t(kt) * frameF + cc;
+        const double fsv = DET ? fxp.scale[0] : 0.0;
+        auto put = [&](size_t idx, float val) {
+            if constexpr (DET) fixed_add(fxp.dvi + idx, val, fsv);
+            else atomicAdd(dv + idx, val);
+        };
         float dwl = 0.f;
         auto body = [&](auto fast_tag) {
             constexpr bool FAST = decltype(fast_tag)::value;
@@ -1069,7 +1086,7 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
                 }
                 if (act) {
 #pragma unroll
-                    for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + colo(j), ka[j]);
+                    for (int j = 0; j <= P; ++j) put(dvo + roa + colo(j), ka[j]);
                 }
 #pragma unroll
                 for (int j = 0; j <= P; ++j) {
@@ -1082,7 +1099,7 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
             }
             if (act) {
 #pragma unroll
-                for (int j = 0; j <= P; ++j) atomicAdd(dvb + roa + colo(j), ka[j]);
+                for (int j = 0; j <= P; ++j) put(dvo + roa + colo(j), ka[j]);
             }
         };
         if (FT > 0 && by >= 0 && by + P < H && bx >= 0 && bx + P < W)  // uniform: one row per warp
@@ -1091,7 +1108,10 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
             body(std::false_type{});
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) dwl += __shfl_xor_sync(0xffffffffu, dwl, m);
-        if (lane == 0) atomicAdd(dw + e, dwl);
+        if (lane == 0) {
+            if constexpr (DET) fixed_add(fxp.dwi + e, dwl, fxp.scale[1]);
+            else atomicAdd(dw + e, dwl);
+        }
     }
 }
 
@@ -1102,27 +1122,61 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
 #define SNLS_WBWD_LSPLIT 2
 #endif
 
-template <int P>
+template <int P, bool DET>
 void launch_wpsum_bwd_rows(const AggArgs& a, const float* go, const int32_t* counts, float* dv,
-                           float* dw, cudaStream_t st) {
-    if (SNLS_WBWD_PAIRS && P >= 5 && (a.d.f == 64 || a.d.f == 32)) {
+                           float* dw, WbwdFixed fxp, cudaStream_t st) {
+    // channel pairs for wide patches (and for every ps in deterministic mode: one dW writer
+    // per entry); the one-channel-per-lane kernel otherwise
+    if (SNLS_WBWD_PAIRS && (P >= 5 || DET) && (a.d.f == 64 || a.d.f == 32)) {
         constexpr int LS = SNLS_WBWD_LSPLIT;
         auto go2 = [&](auto kern, int nl) {
             const size_t smem = size_t(128 / nl) * P * P * nl * sizeof(u64);
             ensure_smem(kern, smem);
             const int64_t units = a.d.rows * LS;
             const unsigned blocks = unsigned((units + 128 / nl - 1) / (128 / nl));
-            kern<<<blocks, 128, smem, st>>>(a, go, counts, dv, dw);
+            kern<<<blocks, 128, smem, st>>>(a, go, counts, dv, dw, fxp);
         };
-        if (a.d.f == 64) go2(wpsum_bwd_pairs<P, 32, LS>, 32);
-        else go2(wpsum_bwd_pairs<P, 16, LS>, 16);
+        if (a.d.f == 64) go2(wpsum_bwd_pairs<P, 32, LS, DET>, 32);
+        else go2(wpsum_bwd_pairs<P, 16, LS, DET>, 16);
         return;
     }
     const int64_t warps = a.d.rows * ((a.d.f + 31) / 32);
     const unsigned blocks = unsigned((warps + 3) / 4);
-    if (a.d.f == 64) wpsum_bwd_rows<P, 64><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
-    else if (a.d.f == 32) wpsum_bwd_rows<P, 32><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
-    else wpsum_bwd_rows<P, 0><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw);
+    if (a.d.f == 64) wpsum_bwd_rows<P, 64, DET><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw, fxp);
+    else if (a.d.f == 32) wpsum_bwd_rows<P, 32, DET><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw, fxp);
+    else wpsum_bwd_rows<P, 0, DET><<<blocks, 128, 0, st>>>(a, go, counts, dv, dw, fxp);
+}
+
+template <bool DET>
+void launch_wpsum_bwd_any(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
+                          float* dw, WbwdFixed fxp, cudaStream_t st) {
+    switch (a.ps) {
+        case 1: launch_wpsum_bwd_rows<1, DET>(a, grad_out, counts, dv, dw, fxp, st); return;
+        case 3: launch_wpsum_bwd_rows<3, DET>(a, grad_out, counts, dv, dw, fxp, st); return;
+        case 5: launch_wpsum_bwd_rows<5, DET>(a, grad_out, counts, dv, dw, fxp, st); return;
+        case 7: launch_wpsum_bwd_rows<7, DET>(a, grad_out, counts, dv, dw, fxp, st); return;
+        default: break;
+    }
+    if (a.d.f % 4 == 0) {
+        const int64_t n = a.d.rows * a.topl * (a.d.f / 4);
+        wpsum_bwd_kernel<4, DET><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, grad_out, counts, dv, dw, fxp);
+    } else {
+        const int64_t n = a.d.rows * a.topl * a.d.f;
+        wpsum_bwd_kernel<1, DET><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, grad_out, counts, dv, dw, fxp);
+    }
+}
+
+// bounds[0..2] = max|grad_out|, max|weights|, max|v| (bits).  Every partial sum of dV is a sum
+// of (row, l, written pixel) terms |g * w * tap| <= max|go| * max|w| (count >= 1, taps <= 1)
+// over at most ps^2 + s0^2 written pixels per (row, l); a dW entry sums <= (ps^2 + s0^2) F
+// terms |g * sample| <= max|go| * max|v|.
+__global__ void wbwd_scales_kernel(const unsigned* bounds, int64_t entries, int ps, int s0, int f,
+                                   double* scales) {
+    const double gm = __uint_as_float(bounds[0]), wm = __uint_as_float(bounds[1]);
+    const double vm = __uint_as_float(bounds[2]);
+    const double px = double(ps) * ps + double(s0) * s0;
+    scales[0] = pow2_scale(double(entries) * px * gm * wm * 1.001);
+    scales[1] = pow2_scale(px * f * gm * vm * 1.001);
 }
 
 }  // namespace
@@ -1164,21 +1218,38 @@ int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st) {
 
 int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                      float* dw, cudaStream_t st) {
-    switch (a.ps) {
-        case 1: launch_wpsum_bwd_rows<1>(a, grad_out, counts, dv, dw, st); return 1;
-        case 3: launch_wpsum_bwd_rows<3>(a, grad_out, counts, dv, dw, st); return 1;
-        case 5: launch_wpsum_bwd_rows<5>(a, grad_out, counts, dv, dw, st); return 1;
-        case 7: launch_wpsum_bwd_rows<7>(a, grad_out, counts, dv, dw, st); return 1;
-        default: break;
-    }
-    if (a.d.f % 4 == 0) {
-        const int64_t n = a.d.rows * a.topl * (a.d.f / 4);
-        wpsum_bwd_kernel<4><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, grad_out, counts, dv, dw);
-    } else {
-        const int64_t n = a.d.rows * a.topl * a.d.f;
-        wpsum_bwd_kernel<1><<<unsigned((n + 255) / 256), 256, 0, st>>>(a, grad_out, counts, dv, dw);
-    }
+    launch_wpsum_bwd_any<false>(a, grad_out, counts, dv, dw, WbwdFixed{nullptr, nullptr, nullptr}, st);
     return 1;
+}
+
+// Deterministic mode (aggregate.cpp:439-450: dV gathered in a fixed order): int64 fixed-point
+// dV (and multi-writer dW) with scales from exact maxima, then one conversion pass.  `work`
+// returns scratch of the requested size (zeroed here).  dv / dw must be zeroed by the caller.
+int launch_wpsum_bwd_det(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
+                         float* dw, const std::function<void*(size_t)>& work, cudaStream_t st) {
+    const int64_t nv = int64_t(a.d.t) * a.d.h * a.d.w * a.d.f;
+    const int64_t ne = a.d.rows * a.topl;
+    const size_t head = 64;  // 2 double scales + 3 uint bounds, padded
+    const size_t bytes = head + size_t(nv + ne) * sizeof(unsigned long long);
+    char* w = static_cast<char*>(work(bytes));
+    if (!w) return -1;
+    cudaMemsetAsync(w, 0, bytes, st);
+    double* scales = reinterpret_cast<double*>(w);
+    unsigned* bounds = reinterpret_cast<unsigned*>(w + 2 * sizeof(double));
+    unsigned long long* dvi = reinterpret_cast<unsigned long long*>(w + head);
+    unsigned long long* dwi = dvi + nv;
+    const int64_t ngo = int64_t(a.d.nt) * a.d.h * a.d.w * a.d.f;
+    absmax_kernel<<<592, 256, 0, st>>>(grad_out, ngo, bounds + 0);
+    absmax_kernel<<<148, 256, 0, st>>>(a.weights, ne, bounds + 1);
+    absmax_kernel<<<592, 256, 0, st>>>(a.v, nv, bounds + 2);
+    wbwd_scales_kernel<<<1, 1, 0, st>>>(bounds, ne, a.ps, a.d.stride0, a.d.f, scales);
+    launch_wpsum_bwd_any<true>(a, grad_out, counts, dv, dw, WbwdFixed{dvi, dwi, scales}, st);
+    fixed_to_float_kernel<<<unsigned(std::min<int64_t>((nv + 255) / 256, 4096)), 256, 0, st>>>(dvi, scales, dv, nv);
+    // the channel-pair kernel writes dW directly (one writer per entry); the others through dwi
+    const bool pairs = SNLS_WBWD_PAIRS && (a.d.f == 64 || a.d.f == 32) && a.ps <= 7 && a.ps % 2 == 1;
+    if (!pairs)
+        fixed_to_float_kernel<<<unsigned(std::min<int64_t>((ne + 255) / 256, 4096)), 256, 0, st>>>(dwi, scales + 1, dw, ne);
+    return pairs ? 7 : 8;
 }
 
 }  // namespace snls_gpu

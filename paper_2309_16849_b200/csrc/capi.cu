@@ -747,6 +747,12 @@ int snls_wpsum_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const 
 int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
                           const float* grad_out, const int32_t* counts, const float* v,
                           const float* weights, const float* offsets, float* dv, float* dw) {
+    return snls_wpsum_bwd_ex(ctx, cfg, dims, t0, t1, grad_out, counts, v, weights, offsets, dv, dw, 0);
+}
+
+int snls_wpsum_bwd_ex(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, int t0, int t1,
+                      const float* grad_out, const int32_t* counts, const float* v,
+                      const float* weights, const float* offsets, float* dv, float* dw, int flags) {
     if (int rc = check_ctx(ctx)) return rc;
     if (int rc = validate(cfg)) return rc;
     if (int rc = check_dims(dims)) return rc;
@@ -754,12 +760,22 @@ int snls_wpsum_bwd_frames(snls_ctx* ctx, const snls_config* cfg, snls_dims dims,
         return fail(SNLS_EARG, "wpsum_backward: null tensor");
     if (t0 < 0 || t1 > dims.t || t0 >= t1)
         return fail(SNLS_EARG, "wpsum_backward: empty or invalid frame range");
+    if (flags & ~SNLS_BWD_DETERMINISTIC) return fail(SNLS_EARG, "wpsum_backward: unknown flags");
     if (int rc = check_aligned("wpsum_backward", {grad_out, v, weights, offsets, dv, dw})) return rc;
     DeviceGuard g(ctx->device);
     const Dims d = restrict_frames(make_dims(dims, cfg->stride0), t0, t1);
     cudaMemsetAsync(dv, 0, size_t(dims.t) * dims.h * dims.w * dims.f * sizeof(float), ctx->stream);
     cudaMemsetAsync(dw, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
     AggArgs a{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err, cfg->wt};
+    if (flags & SNLS_BWD_DETERMINISTIC) {
+        const int n = launch_wpsum_bwd_det(a, grad_out, counts, dv, dw,
+                                           [&](size_t bytes) -> void* {
+                                               return ensure_work(ctx, bytes) ? nullptr : ctx->work;
+                                           },
+                                           ctx->stream);
+        if (n < 0) return fail(SNLS_ECUDA, "wpsum_backward: deterministic workspace");
+        return after_launch(ctx, n, "snls_wpsum_bwd(deterministic)");
+    }
     return after_launch(ctx, launch_wpsum_bwd(a, grad_out, counts, dv, dw, ctx->stream), "snls_wpsum_bwd");
 }
 
@@ -895,11 +911,14 @@ int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const 
                                                    static_cast<double*>(ctx->work), wp, ctx->stream);
         return after_launch(ctx, n, "snls_train_bwd");
     }
-    if (!disjoint || !train_bwd_concurrent())
-        {
-            if (int rc = snls_wpsum_bwd(ctx, cfg, dims, grad_out, counts, v, weights, offsets, dv, dweights)) return rc;
-            return search();
-        }
+    // deterministic: both operators in fixed-point mode, one after the other (they share the
+    // context's workspace)
+    if (!disjoint || !train_bwd_concurrent() || (flags & SNLS_BWD_DETERMINISTIC)) {
+        if (int rc = snls_wpsum_bwd_ex(ctx, cfg, dims, 0, dims.t, grad_out, counts, v, weights, offsets, dv,
+                                       dweights, flags))
+            return rc;
+        return search();
+    }
     if (int rc = check_ctx(ctx)) return rc;
     DeviceGuard g(ctx->device);
     if (!ctx->aux) {

@@ -80,6 +80,10 @@ int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st)
 int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st);
 int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                      float* dw, cudaStream_t st);
+// Deterministic wpsum backward (int64 fixed point; `work` hands out scratch, zeroed there); -1 when
+// the scratch is unavailable.
+int launch_wpsum_bwd_det(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
+                         float* dw, const std::function<void*(size_t)>& work, cudaStream_t st);
 
 // align.cu: block matching (flow.cpp:114-175) over `frames` pairs; per-frame PSNR.
 int launch_block_match(const float* a, const float* b, int frames, int h, int w, int f, int block,

@@ -15,6 +15,7 @@
 #include "kernels.h"
 #include "packed.cuh"
 #include "wpsum_bwd_pairs.cuh"
+#include "fixed_point.cuh"
 
 #ifndef SNLS_BWD_DQSM
 #define SNLS_BWD_DQSM 1
@@ -553,26 +554,6 @@ __global__ void narrow_kernel(const double* __restrict__ a, const double* __rest
 }
 
 // ---- deterministic mode --------------------------------------------------------------
-// Non-negative float maxima (|q|, |k|, |grad|) as uint bit patterns: atomicMax on the bits
-// is exact and order-independent, so the scales below are the same on every run.
-__global__ void absmax_kernel(const float* __restrict__ a, int64_t n, unsigned* out) {
-    float m = 0.f;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        m = fmaxf(m, fabsf(a[i]));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
-}
-
-// 2^(61 - ceil(log2(bound))): |any partial sum| <= bound < 2^61 / scale, so no int64 overflow.
-__device__ __forceinline__ double pow2_scale(double bound) {
-    if (!(bound > 0.0) || !isfinite(bound)) return 1.0;
-    int ex;
-    frexp(bound, &ex);  // bound < 2^ex
-    return ldexp(1.0, 61 - ex);
-}
-
 // bounds[0..2] = max|q|, max|k|, max|grad| (bits).  Per output element and entry, a patch
 // reaches it through at most ps^2 pixels (reflection folds) with tap weights <= 1, so
 // |dQ|, |dK| <= entries * ps^2 * max|g| * max|dS/dq|, max|dS/dk|.
@@ -594,13 +575,6 @@ __global__ void flow_scale_kernel(const unsigned* vmax_bits, int64_t entries, in
     *scale = pow2_scale(double(entries) * (4.0 * (wt > 1 ? wt : 1) + 1.0) * vm * 1.001);
 }
 
-__global__ void fixed_to_float_kernel(const unsigned long long* __restrict__ a, const double* scale,
-                                      float* __restrict__ out, int64_t n) {
-    const double inv = 1.0 / *scale;  // a power of two: exact
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        out[i] = float(double(static_cast<long long>(a[i])) * inv);
-}
 
 }  // namespace
 

@@ -5,6 +5,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "packed.cuh"
+#include "fixed_point.cuh"
 
 namespace snls_gpu {
 namespace {
@@ -34,11 +35,20 @@ __device__ __forceinline__ void red2(float* p, u64 v) {
 // split only adds warps to hide the per-neighbour load latency.
 // The body takes its block index and dynamic shared memory explicitly, so the interleaved
 // training backward (search_bwd.cu train_bwd_interleaved) can run it beside the search backward.
-template <int P, int NL, int LS>
+// DET (deterministic mode): dV (and, where an entry has several writers, dW) accumulate as
+// int64 fixed point (fixed_point.cuh): dvi / dwi with the scales scale[0] / scale[1].  In this
+// kernel dW has one writer per entry in either mode.
+struct WbwdFixed {
+    unsigned long long* dvi;
+    unsigned long long* dwi;
+    const double* scale;
+};
+template <int P, int NL, int LS, bool DET = false>
 __device__ __forceinline__ void wpsum_bwd_pairs_body(const AggArgs& a, const float* __restrict__ go,
                                                      const int32_t* __restrict__ counts,
                                                      float* __restrict__ dv, float* __restrict__ dw,
-                                                     unsigned bid, u64* s_gs2) {  // [128 / NL groups][P * P][NL]
+                                                     unsigned bid, u64* s_gs2,  // [128 / NL groups][P * P][NL]
+                                                     WbwdFixed fxp = {nullptr, nullptr, nullptr}) {
     constexpr int HP = P / 2, F = 2 * NL, GPW = 32 / NL;  // lane groups (rows) per warp
     const int lane = threadIdx.x & 31, c = lane % NL;
     const int grp = threadIdx.x / NL;
@@ -98,7 +108,17 @@ __device__ __forceinline__ void wpsum_bwd_pairs_body(const AggArgs& a, const flo
         const u64 WV = pk2(wv, wv);
         const int by = qy - HP + int_base(fly), bx = qx - HP + int_base(flx);
         const u64* vb = reinterpret_cast<const u64*>(a.v + size_t(kt) * frameF) + c;
-        float* dvb = dv + size_t(kt) * frameF + 2 * c;
+        const size_t dvo = size_t(kt) * frameF + 2 * c;  // this lane's first channel of frame kt
+        const double fsc = DET ? *fxp.scale : 0.0;
+        auto scatter = [&](size_t idx, u64 val) {  // idx: element index of the pair's first channel
+            if constexpr (DET) {
+                const float2 f = upk2(val);
+                fixed_add(fxp.dvi + idx, f.x, fsc);
+                fixed_add(fxp.dvi + idx + 1, f.y, fsc);
+            } else {
+                red2(dv + idx, val);
+            }
+        };
         u64 dwl = 0ull;
         // FAST (block inside the frame): one row base, immediate column offsets j * NL; else
         // reflected rows / columns (tensor.cpp:23-48), the columns resolved once per neighbour
@@ -144,9 +164,8 @@ __device__ __forceinline__ void wpsum_bwd_pairs_body(const AggArgs& a, const flo
                     kn[j] = fma2(gv, W10, kn[j]);
                     kn[j + 1] = fma2(gv, W11, kn[j + 1]);
                 }
-                float* dr = dvb + 2 * roa;
 #pragma unroll
-                for (int j = 0; j <= P; ++j) red2(dr + 2 * colo(j), ka[j]);
+                for (int j = 0; j <= P; ++j) scatter(dvo + 2 * (roa + colo(j)), ka[j]);
 #pragma unroll
                 for (int j = 0; j <= P; ++j) {
                     ra[j] = rb[j];
@@ -156,9 +175,8 @@ __device__ __forceinline__ void wpsum_bwd_pairs_body(const AggArgs& a, const flo
                 roa = rob;
                 rob = ron;
             }
-            float* dr = dvb + 2 * roa;
 #pragma unroll
-            for (int j = 0; j <= P; ++j) red2(dr + 2 * colo(j), ka[j]);
+            for (int j = 0; j <= P; ++j) scatter(dvo + 2 * (roa + colo(j)), ka[j]);
         };
         if (by >= 0 && by + P < H && bx >= 0 && bx + P < W)  // uniform per lane group
             body(std::true_type{});
@@ -168,16 +186,17 @@ __device__ __forceinline__ void wpsum_bwd_pairs_body(const AggArgs& a, const flo
         float dws = d2.x + d2.y;
 #pragma unroll
         for (int m = NL / 2; m >= 1; m >>= 1) dws += __shfl_xor_sync(gmask, dws, m);
-        if (c == 0) atomicAdd(dw + e, dws);
+        if (c == 0) dw[e] = dws;  // the entry's only writer (dw was zeroed: same as an add)
     }
 }
 
-template <int P, int NL, int LS>
+template <int P, int NL, int LS, bool DET = false>
 __global__ void __launch_bounds__(128, 4) wpsum_bwd_pairs(AggArgs a, const float* __restrict__ go,
                                                           const int32_t* __restrict__ counts,
-                                                          float* __restrict__ dv, float* __restrict__ dw) {
+                                                          float* __restrict__ dv, float* __restrict__ dw,
+                                                          WbwdFixed fxp) {
     extern __shared__ u64 s_gs2[];
-    wpsum_bwd_pairs_body<P, NL, LS>(a, go, counts, dv, dw, blockIdx.x, s_gs2);
+    wpsum_bwd_pairs_body<P, NL, LS, DET>(a, go, counts, dv, dw, blockIdx.x, s_gs2, fxp);
 }
 
 }  // namespace

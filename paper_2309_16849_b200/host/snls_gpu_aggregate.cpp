@@ -3,7 +3,8 @@
 // C-ABI.  Validation order and messages follow check_agg_inputs (aggregate.cpp:47-66) and
 // wpsum_backward (aggregate.cpp:415-420); results are charged to memory:: accounting like the
 // reference (aggregate.cpp:136-140, 296).  wpsum always runs as the deterministic gather
-// (either ExecPolicy mode gives the same fixed-order result); the backward uses atomics.
+// (either ExecPolicy mode gives the same fixed-order result); the backward follows
+// ExecPolicy::deterministic (int64 fixed point) or uses atomics.
 #include "snls/aggregate.hpp"
 #include "snls/memory.hpp"
 #include "snls_gpu_runtime.hpp"
@@ -104,7 +105,6 @@ StackedTensor gather_stack(const VideoTensor& v, const WeightTensor& weights,
 AggGradients wpsum_backward(const VideoTensor& grad_out, const AggTape& tape,
                             const VideoTensor& v, const WeightTensor& weights,
                             const OffsetTensor& offsets, const ExecPolicy& policy) {
-    (void)policy;
     if (grad_out.t != tape.t || grad_out.h != tape.h || grad_out.w != tape.w ||
         grad_out.f != tape.f || !grad_out.same_shape(v))
         throw DomainError("wpsum_backward: gradient shape does not match the tape");
@@ -124,7 +124,10 @@ AggGradients wpsum_backward(const VideoTensor& grad_out, const AggTape& tape,
     float* ddv = t_buf.dv.f32(v.size());
     float* ddw = t_buf.dw.f32(weights.values.size());
     const snls_config c = gpu::to_abi(tape.cfg);
-    gpu::check(snls_wpsum_bwd(ctx, &c, dims_of(v), dgo, dcnt, dv, dw, doff, ddv, ddw));
+    // ExecPolicy::deterministic (the reference's default, aggregate.cpp:439-450): int64
+    // fixed-point dV on the device, bitwise identical run to run
+    gpu::check(snls_wpsum_bwd_ex(ctx, &c, dims_of(v), 0, v.t, dgo, dcnt, dv, dw, doff, ddv, ddw,
+                                 policy.deterministic ? SNLS_BWD_DETERMINISTIC : 0));
     gpu::check(snls_ctx_sync_check(ctx));
     gpu::download(g.grad_v.data, ddv, v.size());
     gpu::download(g.grad_weights.values, ddw, weights.values.size());

@@ -153,6 +153,8 @@ def lib() -> C.CDLL:
                 L.snls_search_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 11 + [C.c_int]
                 L.snls_search_tape64.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 5
             L.snls_wpsum_bwd_frames.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7
+            if hasattr(L, "snls_wpsum_bwd_ex"):
+                L.snls_wpsum_bwd_ex.argtypes = [VOIDP, P, _Dims, C.c_int, C.c_int] + [VOIDP] * 7 + [C.c_int]
             L.snls_host_register.argtypes = [VOIDP, C.c_uint64]
             L.snls_host_unregister.argtypes = [VOIDP]
             L.snls_pipeline_create.argtypes = [VOIDP, P, _Dims, C.c_int, C.POINTER(VOIDP)]
@@ -559,9 +561,11 @@ def gather_stack(v, weights, offsets, cfg: SearchConfig, ctx=None, check=True):
 
 
 def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx=None, check=True,
-                   frames=None):
+                   frames=None, deterministic=False):
     """snls::wpsum_backward (aggregate.hpp:83-85) -> (dv, dweights).  `frames=(t0, t1)`:
-    grad_out / counts / weights / offsets hold output frames [t0, t1) only; dv covers v."""
+    grad_out / counts / weights / offsets hold output frames [t0, t1) only; dv covers v.
+    `deterministic`: the reference's ExecPolicy::deterministic (aggregate.cpp:439-450) --
+    bitwise identical results run to run (int64 fixed-point accumulation of dV)."""
     import torch
 
     ctx = ctx or context(v.device.index)
@@ -571,9 +575,9 @@ def wpsum_backward(grad_out, counts, v, weights, offsets, cfg: SearchConfig, ctx
     c = _cfg(cfg)
     dv = torch.empty_like(v)
     dw = torch.empty_like(weights)
-    _raise(lib().snls_wpsum_bwd_frames(ctx.h, C.byref(c), _dims(v), int(t0), int(t1), _ptr(grad_out),
-                                       _ptr(counts), _ptr(v), _ptr(weights), _ptr(offsets), _ptr(dv),
-                                       _ptr(dw)))
+    _raise(lib().snls_wpsum_bwd_ex(ctx.h, C.byref(c), _dims(v), int(t0), int(t1), _ptr(grad_out),
+                                   _ptr(counts), _ptr(v), _ptr(weights), _ptr(offsets), _ptr(dv),
+                                   _ptr(dw), 1 if deterministic else 0))
     if check:
         ctx.sync_check()
     return dv, dw

@@ -98,3 +98,52 @@ def test_train_backward_interleaved_vs_separate_and_oracle(port, ps, f, s0, metr
         err = max_rel(a, b)
         print(f"[train bwd p{ps} f{f} s{s0} {metric}] {name} {err:.2e}")
         assert err <= REL_TOL, (name, err)
+
+
+DET = [(3, 32, 2), (3, 8, 2), (5, 64, 3), (7, 32, 4), (9, 16, 5), (3, 96, 3), (1, 3, 1)]
+
+
+@pytest.mark.parametrize("ps,f,s0", DET, ids=[f"p{p}f{f}s{s}" for p, f, s in DET])
+def test_wpsum_backward_deterministic(port, ps, f, s0):
+    """wpsum_backward in the reference's deterministic mode (aggregate.cpp:439-450; here int64
+    fixed point): bitwise identical on repeated runs and within 1e-5 of the oracle -- through
+    each kernel family (channel pairs, one channel per lane with 1 / 3 slices, the generic
+    per-entry kernel at ps 9)."""
+    S = snls_mod()
+    t, h, w = 3, 23, 21
+    cfg = Cfg(ws=3, wt=1, ps=ps, stride0=s0, topl=4, metric="l2", softmax_scale=1.0)
+    v = video(port, t, h, w, f, 500 + ps + f)
+    wts, offs = _selection(t, h, w, cfg, 13 * ps + s0)
+    _, cnt = S.wpsum(dev(v), dev(wts), dev(offs), scfg(cfg))
+    go = video(port, t, h, w, f, 510 + s0)
+    a = [host(x) for x in S.wpsum_backward(dev(go), cnt, dev(v), dev(wts), dev(offs), scfg(cfg),
+                                           deterministic=True)]
+    b = [host(x) for x in S.wpsum_backward(dev(go), cnt, dev(v), dev(wts), dev(offs), scfg(cfg),
+                                           deterministic=True)]
+    assert all(np.array_equal(x, y) for x, y in zip(a, b)), "deterministic wpsum_backward differs"
+    wdv, wdw = port.wpsum_bwd(go, host(cnt), v, wts, offs, cfg, deterministic=True)
+    edv, edw = max_rel(a[0], wdv), max_rel(a[1], wdw)
+    print(f"[det wpsum bwd p{ps} f{f} s{s0}] dV {edv:.2e} dW {edw:.2e}")
+    assert edv <= REL_TOL and edw <= REL_TOL
+
+
+def test_train_backward_deterministic_is_bitwise_reproducible(port):
+    """snls_train_bwd with SNLS_BWD_DETERMINISTIC: every gradient (dQ, dK, dV, dW, flows)
+    bitwise identical across runs (both operators in fixed-point mode)."""
+    from tests.helpers import flow
+
+    S = snls_mod()
+    t, h, w, f = 4, 21, 19, 64
+    cfg = Cfg(ws=5, wt=2, ps=7, stride0=4, topl=5, metric="ip", softmax_scale=0.05)
+    q, k, v = (video(port, t, h, w, f, 600 + i) for i in range(3))
+    ff, bf = flow(port, t, h, w, 610, 1.5), flow(port, t, h, w, 611, 1.5)
+    r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), want_weights=True)
+    cen, ch = S.search_tape64(r, dev(ff), dev(bf))
+    rows, L = r.sims.shape
+    g = dev(f32(port.uniform(620, -1, 1, rows * L).reshape(rows, L)))
+    _, cnt = S.wpsum(dev(v), r.weights, r.offsets, scfg(cfg))
+    go = dev(video(port, t, h, w, f, 630))
+    runs = [[host(x) for x in S.train_backward(g, go, cnt, r, dev(q), dev(k), dev(v), tape64=(cen, ch),
+                                               deterministic=True)] for _ in range(2)]
+    for x, y, name in zip(runs[0], runs[1], ("dq", "dk", "dv", "dff", "dbf", "dw")):
+        assert np.array_equal(x, y), f"deterministic train_backward {name} differs"

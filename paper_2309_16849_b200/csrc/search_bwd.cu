@@ -431,15 +431,15 @@ void launch_rows(const float* grad, const float* offsets, const float* q, const 
         kern<<<blocks, 128, smem, st>>>(grad, offsets, q, k, d, topl, metric, sq, sk, gyx, centers);
     };
     // compile-time channel counts of the BASELINE shapes (fast interior addressing)
-    const int ft = DET ? 0 : (d.f == 64 ? 64 : (d.f == 32 ? 32 : 0));
+    const int ft = d.f == 64 ? 64 : (d.f == 32 ? 32 : 0);
     const bool ip = metric == SNLS_METRIC_IP;
     if (centers) {
-        if (ft == 64) ip ? go(search_bwd_rows<P, DET, true, DET ? 0 : 64, 1>) : go(search_bwd_rows<P, DET, true, DET ? 0 : 64, 2>);
-        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, true, DET ? 0 : 32, 1>) : go(search_bwd_rows<P, DET, true, DET ? 0 : 32, 2>);
+        if (ft == 64) ip ? go(search_bwd_rows<P, DET, true, 64, 1>) : go(search_bwd_rows<P, DET, true, 64, 2>);
+        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, true, 32, 1>) : go(search_bwd_rows<P, DET, true, 32, 2>);
         else go(search_bwd_rows<P, DET, true, 0>);
     } else {
-        if (ft == 64) ip ? go(search_bwd_rows<P, DET, false, DET ? 0 : 64, 1>) : go(search_bwd_rows<P, DET, false, DET ? 0 : 64, 2>);
-        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, false, DET ? 0 : 32, 1>) : go(search_bwd_rows<P, DET, false, DET ? 0 : 32, 2>);
+        if (ft == 64) ip ? go(search_bwd_rows<P, DET, false, 64, 1>) : go(search_bwd_rows<P, DET, false, 64, 2>);
+        else if (ft == 32) ip ? go(search_bwd_rows<P, DET, false, 32, 1>) : go(search_bwd_rows<P, DET, false, 32, 2>);
         else go(search_bwd_rows<P, DET, false, 0>);
     }
 }

@@ -1225,30 +1225,51 @@ int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* cou
 // Deterministic mode (aggregate.cpp:439-450: dV gathered in a fixed order): int64 fixed-point
 // dV (and multi-writer dW) with scales from exact maxima, then one conversion pass.  `work`
 // returns scratch of the requested size (zeroed here).  dv / dw must be zeroed by the caller.
-int launch_wpsum_bwd_det(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
-                         float* dw, const std::function<void*(size_t)>& work, cudaStream_t st) {
+size_t wpsum_bwd_det_bytes(const AggArgs& a) {
+    const int64_t nv = int64_t(a.d.t) * a.d.h * a.d.w * a.d.f;
+    return 64 + size_t(nv + a.d.rows * a.topl) * sizeof(unsigned long long);
+}
+
+// Zero the scratch `w` (wpsum_bwd_det_bytes), take the exact maxima and the scales; fills the
+// fixed-point sinks of `wp`.
+void wpsum_bwd_det_prep(const AggArgs& a, const float* grad_out, void* w, WpsumBwdArgs& wp, cudaStream_t st) {
     const int64_t nv = int64_t(a.d.t) * a.d.h * a.d.w * a.d.f;
     const int64_t ne = a.d.rows * a.topl;
-    const size_t head = 64;  // 2 double scales + 3 uint bounds, padded
-    const size_t bytes = head + size_t(nv + ne) * sizeof(unsigned long long);
-    char* w = static_cast<char*>(work(bytes));
-    if (!w) return -1;
-    cudaMemsetAsync(w, 0, bytes, st);
-    double* scales = reinterpret_cast<double*>(w);
-    unsigned* bounds = reinterpret_cast<unsigned*>(w + 2 * sizeof(double));
-    unsigned long long* dvi = reinterpret_cast<unsigned long long*>(w + head);
-    unsigned long long* dwi = dvi + nv;
+    char* c = static_cast<char*>(w);
+    cudaMemsetAsync(c, 0, wpsum_bwd_det_bytes(a), st);
+    double* scales = reinterpret_cast<double*>(c);  // [0] dV, [1] dW
+    unsigned* bounds = reinterpret_cast<unsigned*>(c + 2 * sizeof(double));
+    wp.dvi = reinterpret_cast<unsigned long long*>(c + 64);
+    wp.dwi = wp.dvi + nv;
+    wp.scale = scales;
     const int64_t ngo = int64_t(a.d.nt) * a.d.h * a.d.w * a.d.f;
     absmax_kernel<<<592, 256, 0, st>>>(grad_out, ngo, bounds + 0);
     absmax_kernel<<<148, 256, 0, st>>>(a.weights, ne, bounds + 1);
     absmax_kernel<<<592, 256, 0, st>>>(a.v, nv, bounds + 2);
     wbwd_scales_kernel<<<1, 1, 0, st>>>(bounds, ne, a.ps, a.d.stride0, a.d.f, scales);
-    launch_wpsum_bwd_any<true>(a, grad_out, counts, dv, dw, WbwdFixed{dvi, dwi, scales}, st);
-    fixed_to_float_kernel<<<unsigned(std::min<int64_t>((nv + 255) / 256, 4096)), 256, 0, st>>>(dvi, scales, dv, nv);
+}
+
+// Fixed point -> dv (and dw where the kernel that ran had several writers per entry).
+void wpsum_bwd_det_finish(const AggArgs& a, const WpsumBwdArgs& wp, bool dw_direct, cudaStream_t st) {
+    const int64_t nv = int64_t(a.d.t) * a.d.h * a.d.w * a.d.f;
+    const int64_t ne = a.d.rows * a.topl;
+    fixed_to_float_kernel<<<unsigned(std::min<int64_t>((nv + 255) / 256, 4096)), 256, 0, st>>>(wp.dvi, wp.scale,
+                                                                                               wp.dv, nv);
+    if (!dw_direct)
+        fixed_to_float_kernel<<<unsigned(std::min<int64_t>((ne + 255) / 256, 4096)), 256, 0, st>>>(
+            wp.dwi, wp.scale + 1, wp.dw, ne);
+}
+
+int launch_wpsum_bwd_det(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
+                         float* dw, const std::function<void*(size_t)>& work, cudaStream_t st) {
+    void* w = work(wpsum_bwd_det_bytes(a));
+    if (!w) return -1;
+    WpsumBwdArgs wp{a, grad_out, counts, dv, dw, nullptr, nullptr, nullptr};
+    wpsum_bwd_det_prep(a, grad_out, w, wp, st);
+    launch_wpsum_bwd_any<true>(a, grad_out, counts, dv, dw, WbwdFixed{wp.dvi, wp.dwi, wp.scale}, st);
     // the channel-pair kernel writes dW directly (one writer per entry); the others through dwi
     const bool pairs = SNLS_WBWD_PAIRS && (a.d.f == 64 || a.d.f == 32) && a.ps <= 7 && a.ps % 2 == 1;
-    if (!pairs)
-        fixed_to_float_kernel<<<unsigned(std::min<int64_t>((ne + 255) / 256, 4096)), 256, 0, st>>>(dwi, scales + 1, dw, ne);
+    wpsum_bwd_det_finish(a, wp, pairs, st);
     return pairs ? 7 : 8;
 }
 

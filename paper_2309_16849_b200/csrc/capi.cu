@@ -880,7 +880,7 @@ int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const 
                                   dbflow, flags);
     };
     const bool disjoint = dv != dk && dv != dq && (void*)dweights != (void*)dk && (void*)dweights != (void*)dq;
-    if (disjoint && flags == 0 && ctx && cfg && train_bwd_interleavable(cfg->ps, dims.f)) {
+    if (disjoint && (flags & ~SNLS_BWD_DETERMINISTIC) == 0 && ctx && cfg && train_bwd_interleavable(cfg->ps, dims.f)) {
         // one interleaved phase-1 launch (search_bwd.cu train_bwd_interleaved); the checks of
         // both operators first (snls_wpsum_bwd_frames, snls_search_bwd_ex)
         if (int rc = check_ctx(ctx)) return rc;
@@ -900,6 +900,25 @@ int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const 
         cudaMemsetAsync(dk, 0, nv * dims.f * sizeof(float), ctx->stream);
         cudaMemsetAsync(dv, 0, nv * dims.f * sizeof(float), ctx->stream);
         cudaMemsetAsync(dweights, 0, size_t(d.rows) * cfg->topl * sizeof(float), ctx->stream);
+        if (flags & SNLS_BWD_DETERMINISTIC) {
+            // both operators in fixed point, one interleaved phase-1 launch: the search
+            // backward's workspace first, the wpsum backward's after it
+            WpsumBwdArgs wp{AggArgs{v, weights, offsets, d, cfg->ps, cfg->topl, ctx->err, cfg->wt}, grad_out,
+                            counts, dv, dweights, nullptr, nullptr, nullptr};
+            const size_t wbytes = wpsum_bwd_det_bytes(wp.a);
+            auto work = [&](size_t bytes) -> void* {
+                const size_t head = (bytes + 255) & ~size_t(255);
+                if (ensure_work(ctx, head + wbytes)) return nullptr;
+                wpsum_bwd_det_prep(wp.a, grad_out, static_cast<char*>(ctx->work) + head, wp, ctx->stream);
+                return ctx->work;
+            };
+            const int n = launch_search_bwd_det(grad_sims, centers ? nullptr : offsets, centers ? nullptr : chains,
+                                                centers, chains64, q, k, d, cfg->wt, cfg->ps, cfg->topl,
+                                                cfg->metric, dq, dk, dfflow, dbflow, work, ctx->stream, &wp);
+            if (n < 0) return fail(SNLS_ECUDA, "train_backward: deterministic workspace");
+            wpsum_bwd_det_finish(wp.a, wp, /*dw written directly by the channel-pair body*/ true, ctx->stream);
+            return after_launch(ctx, n + 5, "snls_train_bwd(deterministic)");
+        }
         const size_t scratch = (size_t(d.rows) * cfg->topl * 2 + nv * 4) * sizeof(double);
         if (int rc = ensure_work(ctx, scratch)) return rc;
         cudaMemsetAsync(ctx->work, 0, scratch, ctx->stream);

@@ -78,12 +78,29 @@ int launch_softmax(int64_t rows, int l, float beta, const float* sims, float* we
                    cudaStream_t st);
 int launch_wpsum(const AggArgs& a, float* out, int32_t* counts, cudaStream_t st);
 int launch_gather_stack(const AggArgs& a, float* out, cudaStream_t st);
+// The wpsum backward's arguments (the training backward's second operator).
+struct WpsumBwdArgs {
+    AggArgs a;
+    const float* go;
+    const int32_t* counts;
+    float* dv;
+    float* dw;
+    // deterministic mode: int64 fixed-point dV / dW sinks and their scales (device)
+    unsigned long long* dvi;
+    unsigned long long* dwi;
+    const double* scale;
+};
+
 int launch_wpsum_bwd(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                      float* dw, cudaStream_t st);
 // Deterministic wpsum backward (int64 fixed point; `work` hands out scratch, zeroed there); -1 when
 // the scratch is unavailable.
 int launch_wpsum_bwd_det(const AggArgs& a, const float* grad_out, const int32_t* counts, float* dv,
                          float* dw, const std::function<void*(size_t)>& work, cudaStream_t st);
+// its pieces, for the interleaved deterministic training backward
+size_t wpsum_bwd_det_bytes(const AggArgs& a);
+void wpsum_bwd_det_prep(const AggArgs& a, const float* grad_out, void* w, WpsumBwdArgs& wp, cudaStream_t st);
+void wpsum_bwd_det_finish(const AggArgs& a, const WpsumBwdArgs& wp, bool dw_direct, cudaStream_t st);
 
 // align.cu: block matching (flow.cpp:114-175) over `frames` pairs; per-frame PSNR.
 int launch_block_match(const float* a, const float* b, int frames, int h, int w, int f, int block,
@@ -101,13 +118,6 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
 // blocks side by side, search_bwd.cu train_bwd_interleaved), then the search backward's flow
 // route.  `wp`: the wpsum backward's arguments (dv, dw zeroed by the caller).  0 when the
 // shape has no interleaved instantiation (ps 5 / 7 with F 32 / 64).
-struct WpsumBwdArgs {
-    AggArgs a;
-    const float* go;
-    const int32_t* counts;
-    float* dv;
-    float* dw;
-};
 bool train_bwd_interleavable(int ps, int f);
 int launch_train_bwd_interleaved(const float* grad, const float* offsets, const float* chains,
                                  const double* centers, const double* chains64, const float* q,
@@ -118,6 +128,7 @@ int launch_search_bwd_det(const float* grad, const float* offsets, const float* 
                           const double* centers, const double* chains64, const float* q,
                           const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
                           float* dk, float* dff, float* dbf,
-                          const std::function<void*(size_t)>& work, cudaStream_t st);
+                          const std::function<void*(size_t)>& work, cudaStream_t st,
+                          const WpsumBwdArgs* wp = nullptr);  // wp: interleave the wpsum backward
 
 }  // namespace snls_gpu

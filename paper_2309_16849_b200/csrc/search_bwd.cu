@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128, SNLS_BWD_MINB) search_bwd_rows(const floa
 // every SM runs both at once -- the search backward is issue-bound, the wpsum backward waits
 // on its dV reductions through L2 -- instead of one after the other (or overlapping only at
 // the tail when launched on two streams).  Same bodies, same results.
-template <int P, bool CORR, int FT, int MET, int NL, int LS>
+template <int P, bool CORR, int FT, int MET, int NL, int LS, bool DET>
 __global__ void __launch_bounds__(128, SNLS_BWD_MINB) train_bwd_interleaved(
     const float* __restrict__ grad, const float* __restrict__ offsets, const float* __restrict__ q,
     const float* __restrict__ k, Dims d, int topl, Sink sinkq, Sink sinkk, double* __restrict__ gyx,
@@ -413,10 +413,11 @@ __global__ void __launch_bounds__(128, SNLS_BWD_MINB) train_bwd_interleaved(
         idx = b - m;
     }
     if (wp)
-        wpsum_bwd_pairs_body<P, NL, LS>(w.a, w.go, w.counts, w.dv, w.dw, idx, reinterpret_cast<u64*>(s_bwd));
+        wpsum_bwd_pairs_body<P, NL, LS, DET>(w.a, w.go, w.counts, w.dv, w.dw, idx, reinterpret_cast<u64*>(s_bwd),
+                                             WbwdFixed{w.dvi, w.dwi, w.scale});
     else
-        search_bwd_rows_body<P, false, CORR, FT, MET>(grad, offsets, q, k, d, topl, MET - 1, sinkq, sinkk,
-                                                      gyx, centers, idx, s_bwd);
+        search_bwd_rows_body<P, DET, CORR, FT, MET>(grad, offsets, q, k, d, topl, MET - 1, sinkq, sinkk, gyx,
+                                                    centers, idx, s_bwd);
 }
 
 template <int P, bool DET>
@@ -611,7 +612,7 @@ bool train_bwd_interleavable(int ps, int f) {
 }
 
 namespace {
-template <int P, int FT>
+template <int P, int FT, bool DET>
 void launch_interleaved_p(const float* grad, const float* offsets, const double* centers, const float* q,
                           const float* k, Dims d, int topl, int metric, Sink sq, Sink sk, double* gyx,
                           const WpsumBwdArgs& wp, cudaStream_t st) {
@@ -627,9 +628,21 @@ void launch_interleaved_p(const float* grad, const float* offsets, const double*
     };
     const bool ip = metric == SNLS_METRIC_IP;
     if (centers)
-        ip ? go(train_bwd_interleaved<P, true, FT, 1, NL, LS>) : go(train_bwd_interleaved<P, true, FT, 2, NL, LS>);
+        ip ? go(train_bwd_interleaved<P, true, FT, 1, NL, LS, DET>) : go(train_bwd_interleaved<P, true, FT, 2, NL, LS, DET>);
     else
-        ip ? go(train_bwd_interleaved<P, false, FT, 1, NL, LS>) : go(train_bwd_interleaved<P, false, FT, 2, NL, LS>);
+        ip ? go(train_bwd_interleaved<P, false, FT, 1, NL, LS, DET>) : go(train_bwd_interleaved<P, false, FT, 2, NL, LS, DET>);
+}
+
+template <bool DET>
+void launch_interleaved_any(const float* grad, const float* offsets, const double* centers, const float* q,
+                            const float* k, Dims d, int ps, int topl, int metric, Sink sq, Sink sk,
+                            double* gyx, const WpsumBwdArgs& wp, cudaStream_t st) {
+    if (ps == 7)
+        d.f == 64 ? launch_interleaved_p<7, 64, DET>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
+                  : launch_interleaved_p<7, 32, DET>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
+    else
+        d.f == 64 ? launch_interleaved_p<5, 64, DET>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
+                  : launch_interleaved_p<5, 32, DET>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
 }
 }  // namespace
 
@@ -640,12 +653,7 @@ int launch_train_bwd_interleaved(const float* grad, const float* offsets, const 
                                  const WpsumBwdArgs& wp, cudaStream_t st) {
     if (!train_bwd_interleavable(ps, d.f)) return 0;
     const Sink sq{dq, nullptr, nullptr}, sk{dk, nullptr, nullptr};
-    if (ps == 7)
-        d.f == 64 ? launch_interleaved_p<7, 64>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
-                  : launch_interleaved_p<7, 32>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
-    else
-        d.f == 64 ? launch_interleaved_p<5, 64>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st)
-                  : launch_interleaved_p<5, 32>(grad, offsets, centers, q, k, d, topl, metric, sq, sk, gyx, wp, st);
+    launch_interleaved_any<false>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, wp, st);
     double* dff64 = gyx + size_t(d.rows) * topl * 2;
     const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
     double* dbf64 = dff64 + nfl;
@@ -665,7 +673,8 @@ int launch_search_bwd_det(const float* grad, const float* offsets, const float* 
                           const double* centers, const double* chains64, const float* q,
                           const float* k, Dims d, int wt, int ps, int topl, int metric, float* dq,
                           float* dk, float* dff, float* dbf,
-                          const std::function<void*(size_t)>& work, cudaStream_t st) {
+                          const std::function<void*(size_t)>& work, cudaStream_t st,
+                          const WpsumBwdArgs* wp) {
     const int64_t ne = d.rows * topl;
     const int64_t nv = int64_t(d.t) * d.h * d.w * d.f;
     const int64_t nfl = int64_t(d.t) * d.h * d.w * 2;
@@ -689,7 +698,13 @@ int launch_search_bwd_det(const float* grad, const float* offsets, const float* 
     absmax_kernel<<<148, 256, 0, st>>>(grad, ne, bounds + 2);
     bwd_scales_kernel<<<1, 1, 0, st>>>(bounds, ne, ps, metric, scales);
     const Sink sq{nullptr, iq, scales}, sk{nullptr, ik, scales + 1};
-    const int np = launch_phase1<true>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, st);
+    int np;
+    if (wp && train_bwd_interleavable(ps, d.f)) {  // the wpsum backward's blocks beside phase 1
+        launch_interleaved_any<true>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, *wp, st);
+        np = (d.f + 31) / 32;
+    } else {
+        np = launch_phase1<true>(grad, offsets, centers, q, k, d, ps, topl, metric, sq, sk, gyx, st);
+    }
     const unsigned blocks = unsigned((ne + 255) / 256);
     search_bwd_route<1><<<blocks, 256, 0, st>>>(grad, offsets, chains, d, wt, topl, gyx, np, nullptr, nullptr,
                                                  nullptr, nullptr, nullptr, bounds + 3, centers, chains64);

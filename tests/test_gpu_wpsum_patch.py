@@ -147,3 +147,10 @@ def test_train_backward_deterministic_is_bitwise_reproducible(port):
                                                deterministic=True)] for _ in range(2)]
     for x, y, name in zip(runs[0], runs[1], ("dq", "dk", "dv", "dff", "dbf", "dw")):
         assert np.array_equal(x, y), f"deterministic train_backward {name} differs"
+    # the interleaved deterministic launch = the two deterministic operators called separately
+    dq, dk, dff, dbf = [host(x) for x in S.shifted_nls_backward(g, r, dev(q), dev(k), tape64=(cen, ch),
+                                                                 deterministic=True)]
+    dv, dw = [host(x) for x in S.wpsum_backward(go, cnt, dev(v), r.weights, r.offsets, scfg(cfg),
+                                                deterministic=True)]
+    for a, b, name in zip(runs[0], (dq, dk, dv, dff, dbf, dw), ("dq", "dk", "dv", "dff", "dbf", "dw")):
+        assert np.array_equal(a, b), (name, max_rel(a, b))

@@ -88,6 +88,12 @@ def test_null_arguments_rejected_before_any_device_work(S):
     lib.snls_last_error.restype = C.c_char_p
     assert lib.snls_search_fwd(None, None, S._Dims(1, 1, 1, 1), None, None, None, None, 0,
                                None, None, None, None) == 4
+    # the backward entry points (null context first), including the round-2 additions
+    d = S._Dims(1, 1, 1, 1)
+    assert lib.snls_wpsum_bwd_ex(None, None, d, 0, 1, *([None] * 7), 1) == 4
+    assert lib.snls_search_bwd_ex(None, None, d, 0, 1, *([None] * 11), 1) == 4
+    assert lib.snls_train_bwd(None, None, d, *([None] * 17), 1) == 4
+    assert b"context" in lib.snls_last_error()
 
 
 def test_host_gaussian_noise_matches_reference_stream():

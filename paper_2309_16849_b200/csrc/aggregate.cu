@@ -1115,8 +1115,172 @@ __global__ void __launch_bounds__(128, kGsSm ? 4 : 3) wpsum_bwd_rows(AggArgs a, 
     }
 }
 
+// A/B (SNLS_WBWD_WIN=1): the north star's shared-memory pre-reduction for the dV scatter.  One
+// warp per (row, 32-channel slice) as wpsum_bwd_rows; the row's neighbours are taken frame by
+// frame, and when two or more of a frame's raw blocks (all inside the frame) fit a WS x WS
+// window, their contributions are summed in a per-warp shared window (lane = channel, no
+// conflicts) and each touched pixel gets ONE global reduction -- a query's neighbours cluster
+// (scripts/micro/prereduce_potential.py: per (query, frame) the block union is ~half the
+// contributions).  Other blocks scatter directly.  Non-deterministic mode only.
+template <int P, int FT, int WS>
+__global__ void __launch_bounds__(128, 2) wpsum_bwd_win(AggArgs a, const float* __restrict__ go,
+                                                        const int32_t* __restrict__ counts,
+                                                        float* __restrict__ dv, float* __restrict__ dw) {
+    constexpr int HP = P / 2, F = FT, SL = FT / 32;
+    extern __shared__ float s_wb[];  // [4][P*P][32] gradient patch, then [4][WS*WS][32] windows
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (wid >= a.d.rows * SL) return;  // warp-uniform
+    const int64_t row = wid / SL;
+    const int c = int(wid % SL) * 32 + lane;
+    float* sgs = s_wb + size_t(warp) * P * P * 32 + lane;
+    float* win = s_wb + size_t(4) * P * P * 32 + size_t(warp) * WS * WS * 32 + lane;
+    int ti, qy, qx;
+    row_coords(a.d, row, ti, qy, qx);
+    const int H = a.d.h, W = a.d.w, st = a.d.stride0;
+    const size_t rowF = size_t(W) * F, frameF = size_t(H) * rowF;
+    const float* gob = go + size_t(ti - a.d.t0) * frameF + c;
+    const int32_t* cb = counts + size_t(ti - a.d.t0) * H * W;
+    for (int i = 0; i < P; ++i)
+        for (int j = 0; j < P; ++j) {
+            const int y = qy + i - HP, x = qx + j - HP;
+            float v = 0.f;
+            if (y >= 0 && y < H && x >= 0 && x < W) {
+                const int pix = y * W + x;
+                v = __ldg(gob + size_t(pix) * F) * (1.f / float(__ldg(cb + pix)));
+            }
+            sgs[(i * P + j) * 32] = v;
+        }
+    int ylo, yhi, xlo, xhi;
+    cell_span(qy / st, st, a.d.nh, H, ylo, yhi);
+    cell_span(qx / st, st, a.d.nw, W, xlo, xhi);
+    if (ylo < qy - HP || yhi > qy + HP || xlo < qx - HP || xhi > qx + HP) {
+        for (int y = ylo; y <= yhi; ++y)
+            for (int x = xlo; x <= xhi; ++x) {
+                if (abs(y - qy) <= HP && abs(x - qx) <= HP) continue;
+                const int pix = y * W + x;
+                sgs[((clampi(y - qy, HP) + HP) * P + clampi(x - qx, HP) + HP) * 32] +=
+                    __ldg(gob + size_t(pix) * F) * (1.f / float(__ldg(cb + pix)));
+            }
+    }
+    // lane l < topl decodes neighbour l
+    int dkt = -1, dby = 0, dbx = 0;
+    if (lane < a.topl) {
+        const float* o = a.offsets + size_t(row * a.topl + lane) * 3;
+        dkt = ti + int(roundf(__ldg(o)));
+        if (dkt < 0 || dkt >= a.d.t) {
+            latch(a.err, kErrWpsum);
+            dkt = -1;
+        } else {
+            dby = qy - HP + int_base(floorf(__ldg(o + 1)));
+            dbx = qx - HP + int_base(floorf(__ldg(o + 2)));
+        }
+    }
+    const bool inside = dkt >= 0 && dby >= 0 && dby + P < H && dbx >= 0 && dbx + P < W;
+    unsigned remaining = __ballot_sync(0xffffffffu, dkt >= 0);
+    while (remaining) {
+        const int kt0 = __shfl_sync(0xffffffffu, dkt, __ffs(remaining) - 1);
+        const unsigned members = __ballot_sync(0xffffffffu, dkt == kt0) & remaining;
+        remaining &= ~members;
+        const unsigned fm = __ballot_sync(0xffffffffu, inside) & members;
+        const bool mine = (fm >> lane) & 1u;
+        const int y0 = __reduce_min_sync(0xffffffffu, mine ? dby : 0x7fffffff);
+        const int y1 = __reduce_max_sync(0xffffffffu, mine ? dby : -0x7fffffff);
+        const int x0 = __reduce_min_sync(0xffffffffu, mine ? dbx : 0x7fffffff);
+        const int x1 = __reduce_max_sync(0xffffffffu, mine ? dbx : -0x7fffffff);
+        const int BY = y1 - y0 + P + 1, BX = x1 - x0 + P + 1;
+        const bool use_win = __popc(fm) >= 2 && BY <= WS && BX <= WS;
+        if (use_win)
+            for (int k = 0; k < BY * WS; ++k) win[k * 32] = 0.f;
+        for (unsigned mm = members; mm; mm &= mm - 1) {
+            const int l = __ffs(mm) - 1;
+            const int64_t e = row * a.topl + l;
+            const float* o = a.offsets + size_t(e) * 3;
+            const float oy = __ldg(o + 1), ox = __ldg(o + 2);
+            const float fly = floorf(oy), flx = floorf(ox);
+            const float fy = oy - fly, fx = ox - flx;
+            const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+            const float w10 = fy * (1.f - fx), w11 = fy * fx;
+            const float wv = __ldg(a.weights + e);
+            const int by = __shfl_sync(0xffffffffu, dby, l), bx = __shfl_sync(0xffffffffu, dbx, l);
+            const bool fast = (fm >> l) & 1u;
+            const bool towin = use_win && fast;
+            const float* __restrict__ vb = a.v + size_t(kt0) * frameF + c;
+            const size_t dvo = size_t(kt0) * frameF + c;
+            float dwl = 0.f;
+            unsigned bcol[P + 1];
+#pragma unroll
+            for (int j = 0; j <= P; ++j) bcol[j] = unsigned(fast ? bx + j : reflect_near(bx + j, W)) * unsigned(F);
+            auto rowo = [&](int r) -> size_t { return size_t(fast ? by + r : reflect_near(by + r, H)) * rowF; };
+            auto put = [&](int r, size_t ro, int j, float val) {
+                if (towin) win[((by - y0 + r) * WS + (bx - x0 + j)) * 32] += val;
+                else atomicAdd(dv + dvo + ro + bcol[j], val);
+            };
+            float ra[P + 1], rb[P + 1], ka[P + 1], kn[P + 1];
+            size_t roa = rowo(0), rob = rowo(1);
+#pragma unroll
+            for (int j = 0; j <= P; ++j) {
+                ra[j] = __ldg(vb + roa + bcol[j]);
+                rb[j] = __ldg(vb + rob + bcol[j]);
+                ka[j] = 0.f;
+            }
+#pragma unroll 1
+            for (int i = 0; i < P; ++i) {
+                float rn[P + 1];
+                const size_t ron = rowo(i + 2);
+                if (i + 1 < P) {
+#pragma unroll
+                    for (int j = 0; j <= P; ++j) rn[j] = __ldg(vb + ron + bcol[j]);
+                }
+#pragma unroll
+                for (int j = 0; j <= P; ++j) kn[j] = 0.f;
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const float smp = w00 * ra[j] + w01 * ra[j + 1] + w10 * rb[j] + w11 * rb[j + 1];
+                    const float gij = sgs[(i * P + j) * 32];
+                    dwl = fmaf(gij, smp, dwl);
+                    const float gv = gij * wv;
+                    ka[j] += gv * w00;
+                    ka[j + 1] += gv * w01;
+                    kn[j] += gv * w10;
+                    kn[j + 1] += gv * w11;
+                }
+#pragma unroll
+                for (int j = 0; j <= P; ++j) put(i, roa, j, ka[j]);
+#pragma unroll
+                for (int j = 0; j <= P; ++j) {
+                    ra[j] = rb[j];
+                    if (i + 1 < P) rb[j] = rn[j];
+                    ka[j] = kn[j];
+                }
+                roa = rob;
+                rob = ron;
+            }
+#pragma unroll
+            for (int j = 0; j <= P; ++j) put(P, roa, j, ka[j]);
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) dwl += __shfl_xor_sync(0xffffffffu, dwl, m);
+            if (lane == 0) atomicAdd(dw + e, dwl);
+        }
+        if (use_win) {  // one reduction per touched pixel of the window
+            float* drow = dv + size_t(kt0) * frameF + c;
+            for (int r = 0; r < BY; ++r)
+                for (int j = 0; j < BX; ++j) {
+                    const float val = win[(r * WS + j) * 32];
+                    if (val != 0.f) atomicAdd(drow + size_t(y0 + r) * rowF + size_t(x0 + j) * F, val);
+                }
+        }
+    }
+}
+
 #ifndef SNLS_WBWD_PAIRS
 #define SNLS_WBWD_PAIRS 1
+#endif
+#ifndef SNLS_WBWD_WIN
+#define SNLS_WBWD_WIN 0
+#endif
+#ifndef SNLS_WBWD_WS
+#define SNLS_WBWD_WS 12
 #endif
 #ifndef SNLS_WBWD_LSPLIT
 #define SNLS_WBWD_LSPLIT 2
@@ -1127,6 +1291,20 @@ void launch_wpsum_bwd_rows(const AggArgs& a, const float* go, const int32_t* cou
                            float* dw, WbwdFixed fxp, cudaStream_t st) {
     // channel pairs for wide patches (and for every ps in deterministic mode: one dW writer
     // per entry); the one-channel-per-lane kernel otherwise
+    if constexpr (SNLS_WBWD_WIN != 0 && !DET && P >= 5) {  // A/B build only (measured slower)
+      if ((a.d.f == 64 || a.d.f == 32) && a.topl <= 32) {
+        constexpr int WS = SNLS_WBWD_WS;
+          auto go3 = [&](auto kern) {
+              const size_t smem = size_t(4) * (P * P + WS * WS) * 32 * sizeof(float);
+              ensure_smem(kern, smem);
+              const int64_t warps = a.d.rows * (a.d.f / 32);
+              kern<<<unsigned((warps + 3) / 4), 128, smem, st>>>(a, go, counts, dv, dw);
+          };
+          if (a.d.f == 64) go3(wpsum_bwd_win<P, 64, WS>);
+          else go3(wpsum_bwd_win<P, 32, WS>);
+          return;
+      }
+    }
     if (SNLS_WBWD_PAIRS && (P >= 5 || DET) && (a.d.f == 64 || a.d.f == 32)) {
         constexpr int LS = SNLS_WBWD_LSPLIT;
         auto go2 = [&](auto kern, int nl) {

@@ -941,11 +941,7 @@ int snls_train_bwd(snls_ctx* ctx, const snls_config* cfg, snls_dims dims, const 
     if (int rc = check_ctx(ctx)) return rc;
     DeviceGuard g(ctx->device);
     if (!ctx->aux) {
-        static const int prio = [] {  // A/B: stream priority of the wpsum backward
-            const char* e = std::getenv("SNLS_TRAIN_BWD_PRIO");
-            return e ? std::atoi(e) : 0;
-        }();
-        cudaError_t e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio);
+        cudaError_t e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "snls_train_bwd: stream");

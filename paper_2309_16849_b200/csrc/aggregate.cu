@@ -1283,7 +1283,7 @@ __global__ void __launch_bounds__(128, 2) wpsum_bwd_win(AggArgs a, const float* 
 #define SNLS_WBWD_WS 12
 #endif
 #ifndef SNLS_WBWD_LSPLIT
-#define SNLS_WBWD_LSPLIT 2
+#define SNLS_WBWD_LSPLIT 1
 #endif
 
 template <int P, bool DET>

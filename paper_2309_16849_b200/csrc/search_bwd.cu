@@ -601,7 +601,7 @@ int launch_search_bwd_impl(const float* grad, const float* offsets, const float*
 }
 
 #ifndef SNLS_WBWD_LSPLIT_IL
-#define SNLS_WBWD_LSPLIT_IL 2
+#define SNLS_WBWD_LSPLIT_IL 1
 #endif
 bool train_bwd_interleavable(int ps, int f) {
     static const int on = [] {

@@ -29,6 +29,10 @@
 #include "search_select.cuh"
 #include "packed.cuh"
 
+#ifndef SNLS_TILE2D
+#define SNLS_TILE2D 1
+#endif
+
 namespace snls_gpu {
 
 namespace {
@@ -162,7 +166,21 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     // temporally blocked raster, remapped per CTA (its QPB queries stay consecutive in one image
     // row when QPB divides nw): blockIdx-only arithmetic, kept in uniform registers
     const int64_t row0 = BAND ? band_row(a.d, int64_t(blockIdx.x) * C::QPB, a.band) : int64_t(blockIdx.x) * C::QPB;
+#if SNLS_TILE2D
+    // a CTA's queries as a WARPS x QPW tile of the query grid (warp = one query row of QPW
+    // queries) instead of QPB consecutive queries of one image row: the union of their key
+    // regions is smaller (c4 16 queries: 21 x 21 instead of 13 x 45 region pixels per frame),
+    // so more of the raw-row loads hit L1 (c4 search 3.906 -> 3.862 ms; profiles/r01_plans.txt)
+    int64_t row = row_ok ? row0 + qslot : a.d.rows - 1;
+    if (C::QPW > 1 && !BAND && !RP && a.d.nh % C::WARPS == 0 && a.d.nw % C::QPW == 0) {
+        const unsigned tx = unsigned(a.d.nw) / C::QPW, per = tx * (unsigned(a.d.nh) / C::WARPS);
+        const unsigned tl = blockIdx.x / per, rem = blockIdx.x - tl * per;
+        const unsigned ty0 = rem / tx, tx0 = rem - ty0 * tx;
+        row = int64_t(tl) * a.d.nh * a.d.nw + int64_t((ty0 * C::WARPS + warp) * unsigned(a.d.nw) + tx0 * C::QPW + gq);
+    }
+#else
     const int64_t row = row_ok ? row0 + qslot : a.d.rows - 1;
+#endif
     int qt, qy, qx;
     row_coords(a.d, RP ? row / a.topl : row, qt, qy, qx);
     const int H = a.d.h, Wd = a.d.w;

@@ -29,6 +29,9 @@
 #include "search_select.cuh"
 #include "packed.cuh"
 
+#ifndef SNLS_TILE2D_Q1
+#define SNLS_TILE2D_Q1 1
+#endif
 #ifndef SNLS_TILE2D
 #define SNLS_TILE2D 1
 #endif
@@ -178,6 +181,15 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         const unsigned ty0 = rem / tx, tx0 = rem - ty0 * tx;
         row = int64_t(tl) * a.d.nh * a.d.nw + int64_t((ty0 * C::WARPS + warp) * unsigned(a.d.nw) + tx0 * C::QPW + gq);
     }
+#if SNLS_TILE2D_Q1
+    // one query per warp (ps 7): the CTA's 4 queries as a 2 x 2 tile
+    if (C::QPW == 1 && C::WARPS == 4 && !BAND && !RP && a.d.nh % 2 == 0 && a.d.nw % 2 == 0) {
+        const unsigned tx = unsigned(a.d.nw) / 2, per = tx * (unsigned(a.d.nh) / 2);
+        const unsigned tl = blockIdx.x / per, rem = blockIdx.x - tl * per;
+        const unsigned ty0 = rem / tx, tx0 = rem - ty0 * tx;
+        row = int64_t(tl) * a.d.nh * a.d.nw + int64_t((ty0 * 2 + (warp >> 1)) * unsigned(a.d.nw) + tx0 * 2 + (warp & 1));
+    }
+#endif
 #else
     const int64_t row = row_ok ? row0 + qslot : a.d.rows - 1;
 #endif

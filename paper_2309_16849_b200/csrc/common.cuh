@@ -357,7 +357,9 @@ __device__ __forceinline__ void latch(int* err, int bit) {
 // Raise a kernel's dynamic shared-memory limit above the 48 KB default, once per (kernel,
 // device) and size: cudaFuncSetAttribute is a driver call, not something to pay per launch.
 inline void ensure_smem(const void* kern, size_t bytes) {
-    if (bytes <= 48 * 1024) return;
+    // the opt-in covers static + dynamic above 48 KB: ask whenever the dynamic part alone could
+    // push a kernel with static shared memory over the default
+    if (bytes <= 16 * 1024) return;
     int dev = 0;
     cudaGetDevice(&dev);
     static std::mutex m;

@@ -384,9 +384,6 @@ int launch_tiled_agg_any(const AggArgs& a, float* out, int32_t* counts, int stac
 }
 
 // ---- query-centric wpsum ----------------------------------------------------------------
-#ifndef SNLS_WQ_FRAMES
-#define SNLS_WQ_FRAMES 0
-#endif
 #ifndef SNLS_WQ_MINB
 #define SNLS_WQ_MINB 2
 #endif
@@ -421,41 +418,6 @@ __global__ void __launch_bounds__(256, SNLS_WQ_MINB) wpsum_query_kernel(AggArgs 
     const int cg0 = int(blockIdx.y) * G;  // first float4 channel group of this CTA
     const float4* vbase = reinterpret_cast<const float4*>(a.v) + cg0 + gl;
 
-#if SNLS_WQ_FRAMES
-    // frame-major phase A: all groups sweep the key frames in the same order, so the CTA's L1
-    // working set is one frame's region at a time (a group owns its queries' parked patches
-    // and adds each frame's partial sums to them: deterministic, no races)
-    for (int qi = grp; qi < nq; qi += NQG) {
-        float4* dst = s_patch + size_t(qi) * P * P * G + gl;
-#pragma unroll
-        for (int i = 0; i < P * P; ++i) dst[i * G] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    // pass kf = ti - wt .. ti + wt, then one catch-all pass (kf = -1) for offsets reaching
-    // further than the search's wt (wpsum accepts any in-clip offset, aggregate.cpp:108-109)
-    const int kf_lo = max(0, ti - a.wt), kf_hi = min(a.d.t - 1, ti + a.wt);
-    for (int kp = kf_lo; kp <= kf_hi + 1; ++kp)
-    for (int qi = grp; qi < nq; qi += NQG) {
-        const int kf = kp <= kf_hi ? kp : -1;
-        const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
-        const int qy = gy * st, qx = gx * st;
-        const int64_t row = (int64_t(ti) * a.d.nh + gy) * a.d.nw + gx - a.d.row0;
-        float4 acc[P][P];
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-#pragma unroll
-            for (int j = 0; j < P; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        bool any = false;
-        for (int l = 0; l < a.topl; ++l) {
-            const size_t e = size_t(row) * a.topl + l;
-            const float* o = a.offsets + e * 3;
-            int kt = ti + int(roundf(__ldg(o)));
-            if (kt < 0 || kt >= a.d.t) {  // "offsets leave the clip" (aggregate.cpp:108-109)
-                if (kf < 0) latch(a.err, kErrWpsum);
-                continue;
-            }
-            if (kf >= 0 ? kt != kf : (kt >= kf_lo && kt <= kf_hi)) continue;
-            any = true;
-#else
     for (int qi = grp; qi < nq; qi += NQG) {
         const int gy = gy_lo + qi / nqx, gx = gx_lo + qi % nqx;
         const int qy = gy * st, qx = gx * st;
@@ -465,7 +427,7 @@ __global__ void __launch_bounds__(256, SNLS_WQ_MINB) wpsum_query_kernel(AggArgs 
         for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int j = 0; j < P; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int l = 0; l < a.topl; ++l) {
+        auto unit = [&](int l) {
             const size_t e = size_t(row) * a.topl + l;
             const float* o = a.offsets + e * 3;
             int kt = ti + int(roundf(__ldg(o)));
@@ -473,7 +435,6 @@ __global__ void __launch_bounds__(256, SNLS_WQ_MINB) wpsum_query_kernel(AggArgs 
                 latch(a.err, kErrWpsum);
                 kt = ti;
             }
-#endif
             const float oy = __ldg(o + 1), ox = __ldg(o + 2);
             const float fly = floorf(oy), flx = floorf(ox);
             const float fy = oy - fly, fx = ox - flx;
@@ -510,25 +471,13 @@ __global__ void __launch_bounds__(256, SNLS_WQ_MINB) wpsum_query_kernel(AggArgs 
                     c.z = fmaf(w11, D.z, fmaf(w10, C.z, fmaf(w01, B.z, fmaf(w00, A.z, c.z))));
                     c.w = fmaf(w11, D.w, fmaf(w10, C.w, fmaf(w01, B.w, fmaf(w00, A.w, c.w))));
                 }
-        }
+        };
+        for (int l = 0; l < a.topl; ++l) unit(l);
         float4* dst = s_patch + size_t(qi) * P * P * G + gl;
-#if SNLS_WQ_FRAMES
-        if (any) {
-#pragma unroll
-            for (int i = 0; i < P; ++i)
-#pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    float4& d = dst[(i * P + j) * G];
-                    const float4 v = acc[i][j];
-                    d = make_float4(d.x + v.x, d.y + v.y, d.z + v.z, d.w + v.w);
-                }
-        }
-#else
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int j = 0; j < P; ++j) dst[(i * P + j) * G] = acc[i][j];
-#endif
     }
     __syncthreads();
 

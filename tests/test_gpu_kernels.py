@@ -169,3 +169,26 @@ def test_band_raster_is_bitwise_the_plain_raster(port, band):
             outs.append([host(x) for x in (r.sims, r.offsets, r.weights, g.sims)])
         for x, y in zip(*outs):
             assert np.array_equal(x, y)
+
+
+# query grids whose sides divide the CTA tile (the 4 x 4 / 2 x 2 query-tile raster of the tiled
+# plan, search_tiled.cu SNLS_TILE2D*) -- the shapes above mostly take the linear raster
+TILE_SHAPES = [
+    ("c4-tile", 4, 16, 24, 32, Cfg(ws=11, wt=3, ps=3, stride0=2, topl=16, metric="l2", softmax_scale=1.0 / 288)),
+    ("c2-tile", 3, 32, 32, 64, Cfg(ws=9, wt=2, ps=7, stride0=4, topl=10, metric="ip", softmax_scale=1.0 / 3136)),
+    ("c5-tile", 3, 16, 16, 64, Cfg(ws=9, wt=2, ps=3, stride0=2, topl=10, metric="l2", softmax_scale=1.0 / 576)),
+]
+
+
+@pytest.mark.parametrize("name,t,h,w,f,cfg", TILE_SHAPES, ids=[s[0] for s in TILE_SHAPES])
+def test_query_tile_raster_vs_oracle(port, name, t, h, w, f, cfg):
+    S = snls_mod()
+    q = video(port, t, h, w, f, 910)
+    k = q if name != "c2-tile" else video(port, t, h, w, f, 911)
+    ff, bf = flow(port, t, h, w, 912, 2.0), flow(port, t, h, w, 913, 2.0)
+    ref = oracle_ranked(port, q, k, ff, bf, cfg)
+    r = S.shifted_nls_forward(dev(q), dev(k), dev(ff), dev(bf), scfg(cfg), want_weights=True)
+    st = compare_search(r, ref, cfg, q, k, label=f" {name}")
+    assert st["mismatched"] == 0 or st["mismatched"] <= 0.01 * st["rows"]
+    wts = port.softmax_rows(ref["sims"][:, :cfg.topl], cfg.softmax_scale)
+    assert max_rel(host(r.weights), wts) <= REL_TOL

@@ -22,13 +22,24 @@
 //  * Epilogue: G-lane merge keyed on (value desc, slot asc), emit_row (search.cpp:207-234),
 //    chains, and softmax_rows (aggregate.cpp:16-37) when weights are requested.
 // The full ws^2 (2wt+1) score tensor is never materialised, in HBM or shared memory.
+#include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "search_select.cuh"
 #include "packed.cuh"
 
+#ifndef SNLS_XO16
+#define SNLS_XO16 1
+#endif
+#ifndef SNLS_CARVEOUT
+#define SNLS_CARVEOUT -2  // -2: from MINB and the kernel's shared memory; -1: driver default
+#endif
+#ifndef SNLS_KEYS_IN_Q
+#define SNLS_KEYS_IN_Q 1
+#endif
 #ifndef SNLS_TILE2D_Q1
 #define SNLS_TILE2D_Q1 1
 #endif
@@ -155,11 +166,17 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     constexpr int HP = C::HP, HW = C::HW, R = C::R, F = C::F;
     constexpr bool kPackedPath = VEC == 4 && !QREG && kPacked;
     constexpr bool kPairPath = VEC == 2 && !QREG && kQsm;  // Q in shared memory
-    __shared__ uint64_t s_keys[C::QPB][16];
     constexpr bool kQsmF4 = kPackedPath && kQsm4;
+    // the epilogue's key rows live in the query's own (no longer needed) shared-memory patch
+    // when there is one (it holds >= 16 keys): less shared memory per CTA, a larger L1
+    // (float4 path only: on the ps 7 pair path it measured 0.7% slower, c2 0.3536 vs 0.3510 ms)
+    constexpr bool kKeysInQ = SNLS_KEYS_IN_Q && kQsmF4 && size_t(P) * P * G * 16 >= 16 * sizeof(uint64_t);
+    __shared__ uint64_t s_keys[kKeysInQ ? 1 : C::QPB][16];
     // kPairPath: [QPB][P*P][G] channel pairs; kQsmF4: [QPB][P*P][G] float4
     extern __shared__ __align__(16) unsigned char s_qdyn[];
-    __shared__ unsigned s_xo[kXoSmem ? R + 1 : 1][128];
+    // 16-bit when SNLS_XO16 (the launcher requires W * F / VEC < 2^16)
+    using XoT = std::conditional_t<kXoSmem && SNLS_XO16, uint16_t, unsigned>;
+    __shared__ XoT s_xo[kXoSmem ? R + 1 : 1][128];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane / G, gl = lane % G;
@@ -269,17 +286,17 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
         // instead: c4 5.06 vs 4.45 ms) and parked in shared memory: only boundary warps read
         // them, and the R+1 registers go to the interior loop (c4 4.12 -> 4.00 ms, c5 116.9 ->
         // 112.7 ms, c2 0.370 -> 0.357 ms)
-        unsigned xo_r[kXoSmem ? 1 : R + 1];
-        unsigned* xo = kXoSmem ? &s_xo[0][threadIdx.x] : xo_r;
+        XoT xo_r[kXoSmem ? 1 : R + 1];
+        XoT* xo = kXoSmem ? &s_xo[0][threadIdx.x] : xo_r;
         constexpr int XS = kXoSmem ? 128 : 1;  // element stride
         if (kXoSmem) {
             if (!interior) {
 #pragma unroll
-                for (int j = 0; j <= R; ++j) xo[j * XS] = unsigned(reflect_near(bx + j, Wd)) * G;
+                for (int j = 0; j <= R; ++j) xo[j * XS] = XoT(unsigned(reflect_near(bx + j, Wd)) * G);
             }
         } else {
 #pragma unroll
-            for (int j = 0; j <= R; ++j) xo[j] = unsigned(reflect_near(bx + j, Wd)) * G;
+            for (int j = 0; j <= R; ++j) xo[j] = XoT(unsigned(reflect_near(bx + j, Wd)) * G);
         }
         auto ld = [&](unsigned vidx, float (&o)[VEC]) { ldv<VEC>(kframe + size_t(vidx) * VEC, o); };
 
@@ -556,7 +573,13 @@ __global__ void __launch_bounds__(128, MINB) search_tiled_kernel(TiledSearch a) 
     }
 
     if (FG) return;  // selection happens in the top_l pass over the grid
-    sel.emit(a, s_keys[qslot], row, row_ok, gl, qt, qy, qx);
+    if constexpr (kKeysInQ) {
+        __syncwarp();  // the warp's last reads of its query patches are done
+        const size_t qbytes = size_t(P) * P * G * (kQsmF4 ? sizeof(float4) : sizeof(u64));
+        sel.emit(a, reinterpret_cast<uint64_t*>(s_qdyn + size_t(qslot) * qbytes), row, row_ok, gl, qt, qy, qx);
+    } else {
+        sel.emit(a, s_keys[qslot], row, row_ok, gl, qt, qy, qx);
+    }
 }
 
 template <int P, int W, int VEC, int G, int KMAX, int MINB>
@@ -571,6 +594,27 @@ int launch_cfg_b(const TiledSearch& s, cudaStream_t st) {
                             : (VEC == 4 && kQsm4 ? size_t(C::QPB) * P * P * G * sizeof(float4) : 0);
     auto launch = [&](auto kern) {
         ensure_smem(kern, smem);
+        // shared-memory carve-out: just what MINB resident CTAs need, the rest of the 256 KB
+        // stays L1 (c4: 102 KB instead of the driver's 135 KB -> L1 hit 85% -> 88%, search
+        // 3.862 -> 3.824 ms; profiles/r01_plans.txt).  Set once per kernel and device.
+        static int done_dev = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (SNLS_CARVEOUT != -1 && done_dev != dev) {
+            int pct = SNLS_CARVEOUT;
+            if (pct < 0) {
+                cudaFuncAttributes fa{};
+                int per_sm = 0, reserve = 0;
+                cudaFuncGetAttributes(&fa, kern);
+                cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+                cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+                const double need = double(MINB) * double(fa.sharedSizeBytes + smem + size_t(reserve));
+                pct = per_sm > 0 ? int(std::ceil(100.0 * need / per_sm)) : 100;
+                pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
+            }
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            done_dev = dev;
+        }
         kern<<<blocks, 32 * C::WARPS, smem, st>>>(s);
     };
     // the banded raster only where big frames need it (float4 lanes, F = 32 / 64) and the
@@ -702,6 +746,7 @@ int launch_search_tiled(const TiledSearch& s, cudaStream_t st, int* used) {
             return n;
         }
     }
+    if (SNLS_XO16 && int64_t(s.d.w) * s.d.f >= (int64_t(1) << 16)) return 0;  // (16-bit column table)
     if (used) *used = 1;
     if (s.ps == 3 && s.ws == 11) return launch_by_k<3, 11>(s, st);  // c4
     if (s.ps == 3 && s.ws == 9) return launch_by_k<3, 9>(s, st);    // c5
